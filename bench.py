@@ -1,0 +1,466 @@
+#!/usr/bin/env python
+"""Benchmark: fenced-kernel HBM GB/s (% of peak) and overhead vs the unfenced twin.
+
+Workload (BASELINE.json configs[1], "C2"): per GPU one 2^37-byte arena with
+8 tenants x 16 GiB partitions; every step, the multi-tenant launcher issues,
+round-robin over the tenants onto one stream per tenant, each tenant's fenced
+streaming copy of 4 GiB and fenced fp32 SAXPY over 2^30 elements (4 GiB
+tensors).  value = algorithmic bytes of all tenants on all GPUs / step time.
+
+  python bench.py [--gpus N --steps K --warmup W --mode mask|check|none]
+  python bench.py --impl reference      # the CPU oracle on the host cores
+
+Under torchrun (N > 1) every rank runs its own arena (tenants shard across
+GPUs, no data-path collective); the step time is the max over ranks and the
+per-GPU statistics are summed with one NCCL all_reduce.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GiB = 1 << 30
+TENANTS = 8
+PART = 1 << 34                    # 16 GiB
+ARENA = TENANTS * PART            # 2^37
+COPY_BYTES = 1 << 32              # 4 GiB
+SAXPY_N = 1 << 30                 # 2^30 fp32 = 4 GiB per tensor
+OFF_SRC, OFF_DST, OFF_X, OFF_Y = 0, 4 * GiB, 8 * GiB, 12 * GiB
+ALPHA = 1.5
+BYTES_COPY = 2 * COPY_BYTES       # algorithmic bytes per launch
+BYTES_SAXPY = 12 * SAXPY_N
+STEP_BYTES_PER_GPU = TENANTS * (BYTES_COPY + BYTES_SAXPY)
+METRIC = "fenced-kernel HBM GB/s (% of peak) and overhead % vs unfenced, 1/2/4/8 B200"
+WORKLOAD = ("C2: 8 tenants x 16 GiB pow2 partitions per GPU; per tenant fenced copy of 4 GiB + fenced fp32 "
+            "SAXPY over 2^30 elements, issued round-robin on 8 streams by the native launcher")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), float(d.get("bf16_tflops", 1590.0)), \
+            float(d.get("bf16_tflops_sustained", 1400.0)), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return world, rank, local
+
+
+def allreduce(vals, op="max"):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def barrier():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# the GPU arm
+# ---------------------------------------------------------------------------
+
+class Workload:
+    def __init__(self, device: int):
+        import torch
+        from paper_2401_09290_b200 import devmem, guardian as g
+        self.torch, self.g, self.devmem = torch, g, devmem
+        self.device = device
+        self.arena = g.Arena(device, ARENA)
+        self.parts = [self.arena.partition_alloc(PART) for _ in range(TENANTS)]
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(TENANTS)]
+        for t, p in enumerate(self.parts):
+            gen = torch.Generator(device=f"cuda:{device}")
+            gen.manual_seed(1000 * 2 + t)                              # seed = 1000*config + tenant
+            devmem.view(p.base + OFF_SRC, COPY_BYTES // 4, torch.int32, device).random_(generator=gen)
+            devmem.view(p.base + OFF_X, SAXPY_N, torch.float32, device).uniform_(-1.0, 1.0, generator=gen)
+            devmem.view(p.base + OFF_Y, SAXPY_N, torch.float32, device).uniform_(-1.0, 1.0, generator=gen)
+        torch.cuda.synchronize(device)
+
+    def items(self, mode):
+        g = self.g
+        its = []
+        for p in self.parts:
+            its.append(g.work(p.id, g.GD_KIND_COPY, mode, ptr=(p.base + OFF_DST, p.base + OFF_SRC),
+                              u64=(COPY_BYTES,)))
+            its.append(g.work(p.id, g.GD_KIND_SAXPY, mode, ptr=(p.base + OFF_X, p.base + OFF_Y),
+                              u64=(SAXPY_N,), f32=(ALPHA,)))
+        return its
+
+    def step(self, items):
+        return self.arena.launcher_run(items, self.streams)
+
+    def time_steps(self, mode, steps):
+        """Shared start/stop events around `steps` launcher steps (makespan)."""
+        torch = self.torch
+        items = self.items(mode)
+        root = torch.cuda.current_stream(self.device)
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ends = [torch.cuda.Event() for _ in self.streams]
+        barrier()
+        torch.cuda.synchronize(self.device)
+        start.record(root)
+        for s in self.streams:
+            s.wait_event(start)
+        for _ in range(steps):
+            self.step(items)
+        for s, e in zip(self.streams, ends):
+            e.record(s)
+            root.wait_event(e)
+        stop.record(root)
+        torch.cuda.synchronize(self.device)
+        barrier()
+        return start.elapsed_time(stop)                                # ms
+
+    def solo_kernel_ms(self, mode, kind, reps):
+        """Per-launch durations of one kernel launched back-to-back on one
+        stream, CUDA events on that stream (the roofline's denominator)."""
+        torch = self.torch
+        p = self.parts[0]
+        s = self.streams[0]
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                self._launch(kind, mode, p, s)
+            evs[0].record(s)
+            for i in range(reps):
+                self._launch(kind, mode, p, s)
+                evs[i + 1].record(s)
+        torch.cuda.synchronize(self.device)
+        return [evs[i].elapsed_time(evs[i + 1]) for i in range(reps)]
+
+    def _launch(self, kind, mode, p, s):
+        if kind == "copy":
+            self.arena.copy(p.id, mode, p.base + OFF_DST, p.base + OFF_SRC, COPY_BYTES, stream=s)
+        else:
+            self.arena.saxpy(p.id, mode, ALPHA, p.base + OFF_X, p.base + OFF_Y, SAXPY_N, stream=s)
+
+    def e2e(self, mode, steps, warmup):
+        """Through the public API with HOST buffers: every step copies each
+        tenant's inputs host->device (checked transfers, gd_memcpy_h2d), runs
+        the fenced step, and reads the outputs back (gd_memcpy_d2h)."""
+        torch = self.torch
+        host_in = torch.empty(COPY_BYTES, dtype=torch.uint8, pin_memory=True)
+        host_out = torch.empty(COPY_BYTES, dtype=torch.uint8, pin_memory=True)
+        host_in.random_(0, 256)
+        items = self.items(mode)
+        a = self.arena
+
+        def one():
+            for t, p in enumerate(self.parts):
+                s = self.streams[t]
+                for off in (OFF_SRC, OFF_X, OFF_Y):
+                    a.memcpy_h2d(p.id, p.base + off, host_in.data_ptr(), COPY_BYTES, stream=s)
+            self.step(items)
+            for t, p in enumerate(self.parts):
+                s = self.streams[t]
+                for off in (OFF_DST, OFF_Y):
+                    a.memcpy_d2h(p.id, host_out.data_ptr(), p.base + off, COPY_BYTES, stream=s)
+            for s in self.streams:
+                s.synchronize()
+
+        for _ in range(warmup):
+            one()
+        barrier()
+        torch.cuda.synchronize(self.device)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one()
+        torch.cuda.synchronize(self.device)
+        el = time.perf_counter() - t0
+        el = allreduce([el])[0]
+        barrier()
+        return el / steps, 3 * COPY_BYTES * TENANTS, 2 * COPY_BYTES * TENANTS
+
+
+def ncu_traffic(kernel_tag: str):
+    """dram bytes per launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    v = d.get(kernel_tag)
+    return v if isinstance(v, (int, float)) else None
+
+
+def run_gpu(args):
+    import torch
+    world, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    hbm, bf16, bf16s, peak_src = peaks()
+    w = Workload(local)
+
+    for _ in range(args.warmup):
+        w.step(w.items(args.mode))
+    torch.cuda.synchronize(local)
+
+    # ---- the contract's timed region: exactly K steps, max over ranks ----
+    with Clocks(local) as clk:
+        ms = w.time_steps(args.mode, args.steps)
+    ms = allreduce([ms])[0]
+    ms_per_step = ms / args.steps
+    value = world * STEP_BYTES_PER_GPU / (ms_per_step / 1e3) / 1e9
+
+    # ---- overhead vs the unfenced twin: interleaved None/Mask/Check ----
+    per_mode = {"none": [], "mask": [], "check": []}
+    for _ in range(args.reps):
+        for m in ("none", "mask", "check"):
+            per_mode[m].append(allreduce([w.time_steps(m, args.steps)])[0] / args.steps)
+    med = {m: statistics.median(v) for m, v in per_mode.items()}
+    modes_gbs = {m: round(world * STEP_BYTES_PER_GPU / (med[m] / 1e3) / 1e9, 1) for m in med}
+    overhead = {m: round(100.0 * (med[m] / med["none"] - 1.0), 2) for m in ("mask", "check")}
+
+    # ---- roofline of the dominant kernel (saxpy: 12 B/element) ----
+    solo = {}
+    for kind, nbytes in (("saxpy", BYTES_SAXPY), ("copy", BYTES_COPY)):
+        for m in ("none", args.mode):
+            d = w.solo_kernel_ms(m, kind, args.steps)
+            solo[(kind, m)] = (statistics.mean(d), nbytes)
+    sx_ms, sx_bytes = solo[("saxpy", args.mode)]
+    achieved = sx_bytes / (sx_ms / 1e3) / 1e9
+    mode_id = {"none": 0, "mask": 1, "check": 2}[args.mode]
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": ncu_traffic(f"k_saxpy<{mode_id}>"),
+                "kernel": f"k_saxpy<{args.mode}>", "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json)",
+                "bytes_per_launch": sx_bytes, "avg_launch_ms": round(sx_ms, 4),
+                "share_of_step": round(TENANTS * sx_ms / (TENANTS * (sx_ms + solo[("copy", args.mode)][0])), 3)}
+    kernels = {f"{k}/{m}": {"ms": round(t, 4), "GB/s": round(b / (t / 1e3) / 1e9, 1)}
+               for (k, m), (t, b) in solo.items()}
+
+    # ---- end to end through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        s_per_step, h2d, d2h = w.e2e(args.mode, args.e2e_steps, 1)
+        e2e = {"value": round(world * STEP_BYTES_PER_GPU / s_per_step / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": world * h2d, "d2h_bytes_per_step": world * d2h,
+               "steps": args.e2e_steps, "note": "pinned host buffers, checked gd_memcpy_h2d/d2h, PCIe-bound"}
+
+    # ---- statistics reduced over GPUs with NCCL (the one collective) ----
+    st = w.arena.stats()
+    red = allreduce([float(st["violations"]), float(st["launches"]), float(st["bytes"])], op="sum")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(seconds=args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (torch.Generator seeded 1000*2+tenant: random bytes, U[-1,1) fp32)",
+            "config": {"workload": WORKLOAD, "mode": args.mode, "tenants_per_gpu": TENANTS,
+                       "partition_bytes": PART, "copy_bytes": COPY_BYTES, "saxpy_n": SAXPY_N,
+                       "l2": "inputs larger than L2 (4 GiB per tensor vs 126 MB L2), no flush",
+                       "parallelism": f"{world} GPU(s), one arena per GPU, tenants sharded, no data-path collective"},
+            "frac_of_hbm_peak": round(value / world / hbm, 4),
+            "modes_GBps": modes_gbs, "overhead_pct_vs_unfenced": overhead,
+            "roofline": roofline, "kernels_solo": kernels,
+            "e2e": e2e, "gpu_launches": args.steps * 2 * TENANTS,
+            "clocks": clk.summary(),
+            "stats_allreduced": {"violations": int(red[0]), "launches": int(red[1]), "bytes": int(red[2])},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    w.arena.close()
+
+
+# ---------------------------------------------------------------------------
+# the CPU oracle (cpu_baseline leg and --impl reference)
+# ---------------------------------------------------------------------------
+
+SAMPLE_COPY = 64 << 20            # bytes per tenant sample
+SAMPLE_SAXPY = 16 << 20           # elements per tenant sample
+
+
+class OracleSample:
+    """A bounded sample of the C2 workload simulated by the CPU oracle: per
+    tenant a 256 MiB slice of its partition holding a 64 MiB copy and a
+    2^24-element SAXPY (same kernels, same fence, same mode)."""
+
+    def __init__(self, threads: int, mode: str):
+        import numpy as np
+        import oracle
+        import synth
+        self.oracle, self.mode = oracle, mode
+        self.threads = threads
+        self.mems = []
+        for t in range(threads):
+            base = 0x7F0000000000 + t * PART
+            m = oracle.Mem(base, 4 * SAMPLE_COPY)
+            rng = synth.rng_for(1000 * 2 + t)
+            m.buf[:SAMPLE_COPY] = synth.random_bytes(rng, SAMPLE_COPY)
+            m.write(base + 2 * SAMPLE_COPY, synth.uniform_f32(rng, SAMPLE_SAXPY))
+            m.write(base + 3 * SAMPLE_COPY, synth.uniform_f32(rng, SAMPLE_SAXPY))
+            self.mems.append((m, base))
+        self.bytes_per_pass = threads * (2 * SAMPLE_COPY + 12 * SAMPLE_SAXPY)
+
+    def one(self, i):
+        m, base = self.mems[i]
+        o = self.oracle
+        o.copy(m, base, PART, self.mode, base + SAMPLE_COPY, base, SAMPLE_COPY)
+        o.saxpy(m, base, PART, self.mode, ALPHA, base + 2 * SAMPLE_COPY, base + 3 * SAMPLE_COPY, SAMPLE_SAXPY)
+
+    def run_pass(self):
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(self.threads) as ex:
+            list(ex.map(self.one, range(self.threads)))
+
+
+def host_threads():
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    return max(1, min(TENANTS, n))
+
+
+def cpu_baseline(seconds: float = 12.0, mode: str = "mask"):
+    th = host_threads()
+    s = OracleSample(th, mode)
+    t0 = time.perf_counter()
+    passes = 0
+    while True:
+        s.run_pass()
+        passes += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    el = time.perf_counter() - t0
+    return {"value": round(passes * s.bytes_per_pass / el / 1e9, 3), "unit": "GB/s", "cores": th, "kind": "oracle",
+            "sample": f"{passes} pass(es) x {th} tenants x (64 MiB copy + 2^24-element saxpy), mode={mode}, "
+                      f"{el:.1f} s"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    th = host_threads()
+    s = OracleSample(th, args.mode)
+    for _ in range(args.warmup):
+        s.run_pass()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s.run_pass()
+    el = time.perf_counter() - t0
+    value = args.steps * s.bytes_per_pass / el / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * el / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (NumPy PCG64 seeded 1000*2+tenant)",
+        "config": {"workload": WORKLOAD, "mode": args.mode, "tenants_per_gpu": TENANTS,
+                   "partition_bytes": PART, "copy_bytes": COPY_BYTES, "saxpy_n": SAXPY_N,
+                   "parallelism": "host threads, one tenant per thread"},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": th, "kind": "oracle",
+                         "sample": f"per step {th} tenants x (64 MiB copy + 2^24-element saxpy) of the C2 workload"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--mode", default="mask", choices=["none", "mask", "check"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--reps", type=int, default=5, help="interleaved none/mask/check repetitions")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

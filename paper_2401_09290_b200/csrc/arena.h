@@ -1,0 +1,78 @@
+// arena.h -- partition manager internals.
+#pragma once
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <set>
+#include <vector>
+
+#include "guardian.h"
+
+namespace gd {
+
+// Buddy allocator over [0, arena_size) in units of 2^min_order bytes
+// ("base allocated by buddy allocation (guarantees
+// alignment)").  Offsets of order-k blocks are multiples of 2^k; free blocks
+// are coalesced eagerly, so any fully free aligned 2^k region lies inside a
+// single free block of order >= k.  Lowest-address-first within an order.
+class Buddy {
+public:
+    void init(uint64_t arena_size, unsigned min_order);
+    // returns false when no block of 2^order bytes is free
+    bool alloc(unsigned order, uint64_t *off);
+    void free(uint64_t off, unsigned order);
+    uint64_t free_bytes() const;
+    unsigned max_order() const { return max_order_; }
+    unsigned min_order() const { return min_order_; }
+
+private:
+    unsigned min_order_ = 12, max_order_ = 12;
+    std::vector<std::set<uint64_t>> free_;   // free_[order] = offsets
+};
+
+// First-fit sub-allocator inside one partition, 256-byte
+// alignment, exact-address frees.
+class SubAlloc {
+public:
+    void init(uint64_t size);
+    bool alloc(uint64_t bytes, uint64_t *off);
+    bool free(uint64_t off);
+private:
+    std::map<uint64_t, uint64_t> free_;      // offset -> length, disjoint, coalesced
+    std::map<uint64_t, uint64_t> live_;      // offset -> length
+};
+
+struct Partition {
+    bool live = false;
+    uint64_t base = 0, size = 0;
+    unsigned order = 0;
+    SubAlloc sub;
+};
+
+struct HostCounters {
+    uint64_t launches = 0, bytes = 0, flops = 0;
+};
+
+struct Chunk {                      // one physical VMM allocation mapped in the arena
+    unsigned long long handle = 0;  // CUmemGenericAllocationHandle
+    uint64_t size = 0;
+    uint32_t refs = 0;
+};
+
+}  // namespace gd
+
+struct gd_arena {
+    int device = -1;                 // -1: virtual (bookkeeping only)
+    bool vmm = false;                // VA reserved / physical memory mapped by us
+    uint64_t base = 0, size = 0;     // the arena: size pow2, base % size == 0
+    uint64_t reserve_va = 0, reserve_size = 0, gran = 0;
+    std::map<uint64_t, gd::Chunk> chunks;   // chunk VA -> mapping
+    gd::Buddy buddy;
+    gd::Partition parts[GD_MAX_TENANTS];
+    gd::HostCounters host[GD_MAX_TENANTS][GD_NUM_KINDS];
+    unsigned long long *d_stats = nullptr;  // u64[GD_MAX_TENANTS][GD_NUM_KINDS], outside the arena
+    void *zero_buf = nullptr;        // trusted zero row for operands with no rows (gemm.cu)
+    uint64_t zero_bytes = 0;
+    int sms = 148;
+    std::mutex mu;
+};

@@ -1,0 +1,64 @@
+// fence.cuh -- the per-access fence of Guardian (arXiv 2401.09290), sm_100a.
+//
+// One device function per mode, applied to the FINAL effective address of
+// every global access (base+offset forms are materialised first, PAPER.md:232
+// §4.3 second addressing mode).  The partition descriptor reaches the kernel
+// by value as a __grid_constant__ parameter, i.e. in constant bank 0: the
+// paper's "mask and the base partition address" parameters (PAPER.md:175
+// §4.2.3, Listing 1 lines 5-7 and 17-18, reading A12).
+//
+//   MASK : f = (a & mask_w) | base        Listing 1 lines 26-28 (and.b64, or.b64)
+//          mask_w = (size-1) & ~(w-1)      reading A3 (keeps w-alignment)
+//          -> on sm_100 one LOP3 per 32-bit half, operands uniform.
+//   CHECK: ok = ((a - base) & ~mask_w) == 0
+//          <=> a-base in [0, size-w] and a % w == 0 (base is size-aligned)
+//          PAPER.md:175 ("partition base and ending addresses"), 236; A1, A2.
+//          A refused load yields 0, a refused store/atomic is dropped, and
+//          the refusal is counted (aggregated per thread, then per CTA).
+//   NONE : identity (the unfenced twin, "native kernel").
+#pragma once
+#include <cstdint>
+
+#include "fence_desc.h"
+
+namespace gd {
+
+// Per-width precomputation, hoisted out of every loop (uniform values).
+template <int MODE, int W>
+struct Fence {
+    uint64_t base, keep;           // keep = mask & ~(W-1)
+    __device__ __forceinline__ explicit Fence(const FenceDesc &fd)
+        : base(fd.base), keep(fd.mask & ~(uint64_t)(W - 1)) {}
+    // address the access really uses (MASK: fenced; CHECK/NONE: unchanged)
+    __device__ __forceinline__ uint64_t addr(uint64_t a) const {
+        if constexpr (MODE == kMask) return (a & keep) | base;
+        else return a;
+    }
+    // may the access be performed?
+    __device__ __forceinline__ bool ok(uint64_t a) const {
+        if constexpr (MODE == kCheck) return ((a - base) & ~keep) == 0;
+        else return true;
+    }
+};
+
+// Sum a per-thread refusal count over the CTA and add it to the trusted
+// counter with one atomic per CTA.  All threads of the
+// CTA must call it.
+__device__ __forceinline__ void flush_violations(uint32_t nv_thread, unsigned long long *viol) {
+    __shared__ unsigned long long warp_sums[32];
+    uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    unsigned long long nv = nv_thread;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
+    if (lane == 0) warp_sums[warp] = nv;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t nw = (blockDim.x + 31u) >> 5;
+        unsigned long long s = lane < nw ? warp_sums[lane] : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0 && s) atomicAdd(viol, s);
+    }
+}
+
+}  // namespace gd

@@ -1,0 +1,292 @@
+// gemm.cu -- fenced bf16 GEMM C = A . B^T on the sm_100a tensor cores
+// (SURVEY.md §2.7 K6, §8(a) a9).
+//
+// The fence of a TMA path lives in the tensor maps (there is no per-element
+// address to fence once TMA moves whole tiles):
+//   MASK : the operand's global address is fenced like a 16-byte access,
+//          A' = (A & ((size-1) & ~15)) | base (Listing 1 lines 26-28);
+//   CHECK: A' = A if A is a legal 16-byte-aligned address of the partition,
+//          otherwise the operand has no rows;
+//   then the row extent is clamped so the last byte of the last row lies
+//   below end: rows = min(R, floor((end - A' - rowbytes) / stride) + 1).
+// TMA zero-fills rows at or past that extent, so clamped rows of A / B read
+// as zeros; rows of C at or past its extent are not stored.  Check mode
+// counts the refused rows, (M - rowsA) + (N - rowsB) + (M - rowsC).
+// Same principle as the per-access fence; sm_86 has no
+// TMA, so the paper has no passage for it (reading R-TMA).
+//
+// Kernel: one 128 x 256 output tile per CTA; warp 0 = TMA producer (one
+// elected thread, 4-stage mbarrier ring of 48 KB stages, 128-byte swizzle),
+// warp 1 = MMA issuer (one thread: tcgen05.mma.cta_group::1.kind::f16,
+// M=128 N=256 K=16, fp32 accumulator in TMEM, 256 columns), warp 2 = TMEM
+// allocator, warps 4-7 = epilogue (tcgen05.ld 32x32b -> bf16 -> st.global,
+// rows clamped to the C extent).  All waits are bounded: a kernel that
+// cannot make progress sets a device error word and exits instead of hanging
+// the shared context.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstring>
+
+#include "dispatch.h"
+#include "drv.h"
+
+namespace gd {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr uint32_t A_BYTES = BM * BK * 2;          // 16 KB
+constexpr uint32_t B_BYTES = BN * BK * 2;          // 32 KB
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int THREADS = 256;
+constexpr uint32_t TMEM_COLS = 256;
+
+// instruction descriptor: D f32, A/B bf16, both K-major, N=256, M=128
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ unsigned int g_gemm_timeout = 0;        // set if a bounded wait expired
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ bool mbar_wait(uint32_t bar, uint32_t parity) {
+    for (uint32_t spin = 0; spin < (1u << 26); spin++) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity), "r"(0x989680u)
+            : "memory");
+        if (done) return true;
+    }
+    atomicExch(&g_gemm_timeout, 1u);
+    return false;
+}
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    // UMMA shared-memory descriptor, K-major, 128-byte swizzle: start >> 4,
+    // LBO = 16 B (unused), SBO = 1024 B (8 rows x 128 B), version 1, layout 2.
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, uint64_t C, uint64_t ldc,
+       uint32_t N, uint32_t K, uint64_t rowsC) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *bars = (uint64_t *)(smem + STAGES * STAGE_BYTES);
+    uint64_t *full = bars, *empty = bars + STAGES, *tmem_full = bars + 2 * STAGES;
+    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * STAGES + 1);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const uint32_t nkb = K / BK;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+        for (int s = 0; s < STAGES; s++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
+        }
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(tmem_full)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer ----------------
+        for (uint32_t kb = 0; kb < nkb; kb++) {
+            const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1;
+            if (!mbar_wait(smem_u32(&empty[s]), ph ^ 1)) break;
+            const uint32_t fb = smem_u32(&full[s]);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(STAGE_BYTES)
+                         : "memory");
+            const uint32_t sa = smem_u32(smem + s * STAGE_BYTES), sb = sa + A_BYTES;
+            const int kc = (int)(kb * BK);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                ::"r"(sa), "l"(&tmA), "r"(fb), "r"(kc), "r"((int)m0)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                ::"r"(sb), "l"(&tmB), "r"(fb), "r"(kc), "r"((int)n0)
+                : "memory");
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer ----------------
+        for (uint32_t kb = 0; kb < nkb; kb++) {
+            const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1;
+            if (!mbar_wait(smem_u32(&full[s]), ph)) break;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t sa = smem_u32(smem + s * STAGE_BYTES), sb = sa + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; k++) {
+                const uint64_t da = sw128_desc(sa + 32 * k), db = sw128_desc(sb + 32 * k);
+                const uint32_t acc = (kb | k) ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                    ::"r"(tmem), "l"(da), "l"(db), "r"(IDESC), "r"(acc)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                         ::"r"(smem_u32(&empty[s]))
+                         : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     ::"r"(smem_u32(tmem_full))
+                     : "memory");
+    } else if (warp >= 4) {
+        // ---------------- epilogue: TMEM -> registers -> bf16 -> global ----------------
+        const uint32_t wq = warp - 4;                  // TMEM lanes 32*wq .. 32*wq+31
+        const bool ok = mbar_wait(smem_u32(tmem_full), 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t row = (uint64_t)m0 + wq * 32 + lane;
+        const bool store_row = ok && row < rowsC;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; c++) {
+            uint32_t v[32];
+            const uint32_t taddr = tmem + ((wq * 32u) << 16) + (uint32_t)(c * 32);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (store_row) {
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const uint32_t col = n0 + c * 32 + q * 8;
+                    if (col < N) {
+                        uint32_t p[4];
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * e]),
+                                                                     __uint_as_float(v[q * 8 + 2 * e + 1]));
+                            p[e] = *reinterpret_cast<uint32_t *>(&h);
+                        }
+                        uint4 *dst = reinterpret_cast<uint4 *>(C + 2 * (row * ldc + col));
+                        *dst = make_uint4(p[0], p[1], p[2], p[3]);
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 2) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+__global__ void k_add_violations(unsigned long long *viol, unsigned long long n) { atomicAdd(viol, n); }
+
+// 2-D bf16 tensor map: inner dim = K (contiguous), outer = rows.
+bool make_map(CUtensorMap *m, uint64_t addr, uint64_t K, uint64_t rows, uint64_t ld, uint32_t box_rows) {
+    const cuuint64_t dims[2] = {K, rows};
+    const cuuint64_t strides[1] = {ld * 2};
+    const cuuint32_t box[2] = {BK, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = drv().TensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void *)addr, dims, strides, box,
+                                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// Host side of the descriptor fence (reading R-TMA).
+uint64_t desc_rows(int mode, uint64_t base, uint64_t size, uint64_t p, uint64_t rows, uint64_t rowbytes,
+                   uint64_t stride, uint64_t *pf) {
+    *pf = p;
+    if (mode == kNone) return rows;
+    const uint64_t keep = (size - 1) & ~15ull;
+    uint64_t f;
+    if (mode == kMask) {
+        f = (p & keep) | base;
+    } else {
+        if (((p - base) & ~keep) != 0) return 0;      // not a legal 16-byte access of the partition
+        f = p;
+    }
+    *pf = f;
+    const uint64_t end = base + size;
+    if (end - f < rowbytes) return 0;
+    const uint64_t valid = (end - f - rowbytes) / stride + 1;
+    return valid < rows ? valid : rows;
+}
+
+gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t size, cudaStream_t s,
+                        const Geom &) {
+    const uint32_t M = w.u32[0], N = w.u32[1], K = w.u32[2];
+    const uint64_t lda = w.u64[0], ldb = w.u64[1], ldc = w.u64[2];
+    uint64_t Af, Bf, Cf;
+    uint64_t rA = desc_rows(w.mode, base, size, w.ptr[1], M, 2ull * K, 2ull * lda, &Af);
+    uint64_t rB = desc_rows(w.mode, base, size, w.ptr[2], N, 2ull * K, 2ull * ldb, &Bf);
+    const uint64_t rC = desc_rows(w.mode, base, size, w.ptr[0], M, 2ull * N, 2ull * ldc, &Cf);
+    if (w.mode == kCheck) {
+        const unsigned long long nv = (M - rA) + (N - rB) + (M - rC);
+        if (nv) {
+            k_add_violations<<<1, 1, 0, s>>>(a->d_stats + (uint64_t)w.tenant * GD_NUM_KINDS + GD_KIND_GEMM, nv);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_status(e);
+        }
+    }
+    if (rC == 0) return GD_OK;                         // nothing may be stored
+    if (rA == 0 || rB == 0) {
+        // an operand with no rows reads as zeros: point its map at a trusted
+        // zero row outside every partition
+        std::lock_guard<std::mutex> lk(a->mu);
+        if (a->zero_bytes < 2ull * K) {
+            if (a->zero_buf) cudaFree(a->zero_buf);
+            a->zero_buf = nullptr;
+            a->zero_bytes = 0;
+            cudaError_t e = cudaMalloc(&a->zero_buf, 2ull * K);
+            if (e == cudaSuccess) e = cudaMemset(a->zero_buf, 0, 2ull * K);
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) return cuda_status(e);
+            a->zero_bytes = 2ull * K;
+        }
+        if (rA == 0) { Af = (uint64_t)a->zero_buf; rA = 1; }
+        if (rB == 0) { Bf = (uint64_t)a->zero_buf; rB = 1; }
+    }
+    CUtensorMap tmA, tmB;
+    std::memset(&tmA, 0, sizeof(tmA));
+    std::memset(&tmB, 0, sizeof(tmB));
+    const uint64_t ldA = (Af == (uint64_t)a->zero_buf) ? K : lda, ldB = (Bf == (uint64_t)a->zero_buf) ? K : ldb;
+    if (!make_map(&tmA, Af, K, rA, ldA, BM) || !make_map(&tmB, Bf, K, rB, ldB, BN)) return GD_ERR_UNSUPPORTED;
+    static bool attr = [] {
+        return cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) == cudaSuccess;
+    }();
+    if (!attr) return cuda_status(cudaErrorInvalidValue);
+    const uint32_t rows = (uint32_t)rC;                // rC <= M
+    const dim3 grid((N + BN - 1) / BN, (rows + BM - 1) / BM);
+    k_gemm<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, Cf, ldc, N, K, rC);
+    return cuda_status(cudaGetLastError());
+}
+
+// Read-and-clear the device timeout flag (tests use it to detect a stalled pipeline).
+unsigned int gemm_timeout_flag() {
+    unsigned int v = 0, z = 0;
+    cudaMemcpyFromSymbol(&v, g_gemm_timeout, sizeof(v));
+    cudaMemcpyToSymbol(g_gemm_timeout, &z, sizeof(z));
+    return v;
+}
+
+}  // namespace gd

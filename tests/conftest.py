@@ -18,3 +18,22 @@ def oracle_lib():
     import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture
+def arenas():
+    """Factory of VMM arenas on cuda:0, all destroyed at teardown."""
+    import torch
+    from paper_2401_09290_b200 import guardian as g
+    made = []
+
+    def make(nbytes):
+        a = g.Arena(0, nbytes)
+        made.append(a)
+        return a
+
+    yield make
+    torch.cuda.synchronize()
+    for a in made:
+        a.close()
+    torch.cuda.empty_cache()

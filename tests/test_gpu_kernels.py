@@ -1,0 +1,367 @@
+"""GPU parity: every fenced kernel against the CPU oracle, element by element.
+
+Sizes here span many CTAs / tiles plus a ragged tail; each test compares the
+WHOLE tenant partition byte for byte with the oracle's simulation of the
+same partition, checks the violation counter exactly, and checks that every
+other partition of the arena (the victims) is bit-identical before/after.
+Called through the C ABI (paper_2401_09290_b200.guardian).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2401_09290_b200 import guardian as g
+from tests.gpu_util import download, first_diff, upload
+
+pytestmark = pytest.mark.gpu
+
+MiB = 1 << 20
+PART = 16 * MiB
+MODES = ["none", "mask", "check"]
+
+
+def _setup(arenas, seed=0, tenants=4):
+    a = arenas(tenants * PART)
+    parts = [a.partition_alloc(PART) for _ in range(tenants)]
+    rng = synth.rng_for(seed)
+    # every partition gets random content, so victims have something to lose
+    for p in parts:
+        upload(p.base, synth.random_bytes(rng, PART))
+    return a, parts, rng
+
+
+def _run(a, parts, t, mode, launch, oracle_fn, expect_violations=None):
+    """Launch on tenant t, simulate the same in the oracle, compare."""
+    p = parts[t]
+    whole_before = download(a.base, a.size)
+    a.stats_reset()
+    launch(p)
+    st = a.stats(p.id)
+    whole_after = download(a.base, a.size)
+    lo = p.base - a.base
+    mem = oracle.Mem(p.base, buf=whole_before[lo:lo + p.size].copy())
+    c = oracle_fn(mem, p)
+    got = whole_after[lo:lo + p.size]
+    assert np.array_equal(got, mem.buf), f"{mode}: partition differs from oracle: {first_diff(got, mem.buf)}"
+    assert np.array_equal(whole_after[:lo], whole_before[:lo]), "victim partitions below were modified"
+    assert np.array_equal(whole_after[lo + p.size:], whole_before[lo + p.size:]), "victims above were modified"
+    assert c.faults == 0
+    assert st["violations"] == c.violations, (st["violations"], c.violations)
+    if expect_violations is not None:
+        assert c.violations == expect_violations
+    return st, c
+
+
+# ---------------------------------------------------------------------------
+# K1 copy
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("n", [0, 5, 16, 3 * MiB + 16 * 37 + 11])
+def test_copy_in_bounds(arenas, mode, n):
+    a, parts, _ = _setup(arenas, seed=1)
+    src, dst = 1 * MiB, 8 * MiB
+    _run(a, parts, 1, mode,
+         lambda p: a.copy(p.id, mode, p.base + dst, p.base + src, n),
+         lambda m, p: oracle.copy(m, p.base, p.size, mode, p.base + dst, p.base + src, n), 0)
+
+
+@pytest.mark.parametrize("mode", ["mask", "check"])
+def test_copy_crossing_end(arenas, mode):
+    """dst's last `over` bytes lie past end: mask wraps them to [base, base+over),
+    check refuses exactly those stores (SURVEY.md §8(d) C2 parity variant)."""
+    a, parts, _ = _setup(arenas, seed=2)
+    n, over = 2 * MiB + 16 * 5 + 3, 256 * 1024 + 16 * 3 + 3
+    src = 1 * MiB
+    _run(a, parts, 2, mode,
+         lambda p: a.copy(p.id, mode, p.end - (n - over), p.base + src, n),
+         lambda m, p: oracle.copy(m, p.base, p.size, mode, p.end - (n - over), p.base + src, n),
+         None if mode == "mask" else (over - 3) // 16 + 3)
+
+
+@pytest.mark.parametrize("mode", ["mask", "check"])
+def test_copy_from_victim(arenas, mode):
+    """src points into another tenant's partition: mask reads the own
+    partition at the wrapped offset (Figure 4), check reads zeros."""
+    a, parts, _ = _setup(arenas, seed=3)
+    n = MiB + 48
+    _run(a, parts, 1, mode,
+         lambda p: a.copy(p.id, mode, p.base + 8 * MiB, parts[0].base + 2 * MiB, n),
+         lambda m, p: oracle.copy(m, p.base, p.size, mode, p.base + 8 * MiB, parts[0].base + 2 * MiB, n),
+         None if mode == "mask" else (n // 16))
+
+
+def test_copy_rejects_misaligned(arenas):
+    a, parts, _ = _setup(arenas, seed=4)
+    with pytest.raises(g.GuardianError) as e:
+        a.copy(parts[0].id, "mask", parts[0].base + 8, parts[0].base, 64)
+    assert e.value.status == g.GD_ERR_ALIGN
+
+
+# ---------------------------------------------------------------------------
+# K2 saxpy
+# ---------------------------------------------------------------------------
+
+def _saxpy_setup(a, parts, rng, n, x_off, y_off, t):
+    p = parts[t]
+    upload(p.base + x_off, synth.uniform_f32(rng, n))
+    upload(p.base + y_off, synth.uniform_f32(rng, n))
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("n", [3, 1 << 20, (1 << 20) + 4 * 999 + 3])
+def test_saxpy_in_bounds(arenas, mode, n):
+    a, parts, rng = _setup(arenas, seed=5)
+    x, y = 1 * MiB, 8 * MiB
+    _saxpy_setup(a, parts, rng, n, x, y, 1)
+    _run(a, parts, 1, mode,
+         lambda p: a.saxpy(p.id, mode, 1.5, p.base + x, p.base + y, n),
+         lambda m, p: oracle.saxpy(m, p.base, p.size, mode, 1.5, p.base + x, p.base + y, n), 0)
+
+
+@pytest.mark.parametrize("mode", ["mask", "check"])
+def test_saxpy_crossing_end(arenas, mode):
+    a, parts, rng = _setup(arenas, seed=6)
+    n, over = (1 << 19) + 7, (1 << 16) + 3       # elements past end
+    x = 1 * MiB
+    p = parts[3]
+    upload(p.base + x, synth.uniform_f32(rng, n))
+    y = p.end - 4 * (n - over)
+    # finite floats wherever y's elements (in place or wrapped) live: IEEE 754
+    # does not fix NaN payload propagation, so inputs are NaN-free
+    upload(y, synth.uniform_f32(rng, n - over))
+    upload(p.base, synth.uniform_f32(rng, over))
+    _run(a, parts, 3, mode,
+         lambda p: a.saxpy(p.id, mode, -0.75, p.base + x, y, n),
+         lambda m, p: oracle.saxpy(m, p.base, p.size, mode, -0.75, p.base + x, y, n),
+         None if mode == "mask" else 2 * over)
+
+
+# ---------------------------------------------------------------------------
+# K3 gather / K4 scatter-add
+# ---------------------------------------------------------------------------
+
+TAB_N = 1 << 20            # 4 MiB table at offset 0
+IDX_OFF, OUT_OFF = 4 * MiB, 6 * MiB
+PAT_LO = 10 * MiB          # wrapped accesses land in [10 MiB, 16 MiB): nothing else touches it
+
+
+def _gather_inputs(rng, n, frac, D=1):
+    j = rng.integers(0, TAB_N // D, n, dtype=np.int64).astype(np.int32)
+    k = synth.planted_count(frac, n)
+    pos = synth.planted_positions(rng, n, k)
+    if k and D == 1:
+        j[pos] = synth.oob_indices(rng, k, PART // 4, PAT_LO // 4, PART // 4)
+    elif k:
+        # whole row outside the partition, its wrapped image inside [PAT_LO, PART)
+        got = []
+        while len(got) < k:
+            c = rng.integers(-(2**31) // D, (2**31 - 1) // D, 4 * k, dtype=np.int64)
+            raw = 4 * c * D
+            res = np.mod(raw, PART)
+            ok = ((raw + 4 * D <= 0) | (raw >= PART)) & (res >= PAT_LO) & (res <= PART - 4 * D)
+            got.extend(c[ok].tolist())
+        j[pos] = np.array(got[:k], dtype=np.int64).astype(np.int32)
+    return j, pos
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("n", [1, 7, (1 << 18) + 3])
+def test_gather_in_bounds(arenas, mode, n):
+    a, parts, rng = _setup(arenas, seed=7)
+    p = parts[1]
+    j, _ = _gather_inputs(rng, n, 0.0)
+    upload(p.base + IDX_OFF, j)
+    _run(a, parts, 1, mode,
+         lambda p: a.gather(p.id, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, n),
+         lambda m, p: oracle.gather(m, p.base, p.size, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, n), 0)
+
+
+@pytest.mark.parametrize("mode", ["mask", "check"])
+@pytest.mark.parametrize("frac", [0.01, 0.1])
+def test_gather_adversarial(arenas, mode, frac):
+    a, parts, rng = _setup(arenas, seed=8)
+    n = (1 << 18) + 1
+    p = parts[2]
+    j, pos = _gather_inputs(rng, n, frac)
+    upload(p.base + IDX_OFF, j)
+    _run(a, parts, 2, mode,
+         lambda p: a.gather(p.id, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, n),
+         lambda m, p: oracle.gather(m, p.base, p.size, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, n),
+         None if mode == "mask" else len(pos))
+
+
+@pytest.mark.parametrize("mode", MODES[1:])
+@pytest.mark.parametrize("D", [2, 3, 33])
+def test_gather_rows(arenas, mode, D):
+    a, parts, rng = _setup(arenas, seed=9)
+    n = 5000 + D
+    p = parts[1]
+    j, pos = _gather_inputs(rng, n, 0.02, D)
+    upload(p.base + IDX_OFF, j)
+    _run(a, parts, 1, mode,
+         lambda p: a.gather(p.id, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, n, D),
+         lambda m, p: oracle.gather(m, p.base, p.size, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, n, D),
+         None if mode == "mask" else len(pos) * D)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_scatter_add(arenas, mode):
+    a, parts, rng = _setup(arenas, seed=10)
+    n = (1 << 18) + 2
+    p = parts[1]
+    j = rng.integers(0, 4096, n, dtype=np.int64).astype(np.int32)     # heavy duplication
+    if mode != "none":
+        k = synth.planted_count(0.05, n)
+        pos = synth.planted_positions(rng, n, k)
+        j[pos] = synth.oob_indices(rng, k, PART // 4, PAT_LO // 4, PART // 4)
+    upload(p.base + IDX_OFF, j)
+    _run(a, parts, 1, mode,
+         lambda p: a.scatter(p.id, mode, p.base, p.base + IDX_OFF, p.base + OUT_OFF, n),
+         lambda m, p: oracle.scatter_add(m, p.base, p.size, mode, p.base, p.base + IDX_OFF, p.base + OUT_OFF, n))
+
+
+# ---------------------------------------------------------------------------
+# K5 stencil
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("H,W,pitch", [(3, 3, 4), (67, 203, 208), (300, 1100, 1104), (130, 4, 4)])
+def test_stencil(arenas, mode, H, W, pitch):
+    a, parts, rng = _setup(arenas, seed=11)
+    p = parts[1]
+    inp, out = 1 * MiB, 8 * MiB
+    upload(p.base + inp, synth.uniform_f32(rng, H * pitch, 0.0, 1.0))
+    _run(a, parts, 1, mode,
+         lambda p: a.stencil(p.id, mode, p.base + out, p.base + inp, H, W, pitch, 0.5, 0.125),
+         lambda m, p: oracle.stencil(m, p.base, p.size, mode, p.base + out, p.base + inp, H, W, pitch, 0.5, 0.125),
+         0)
+
+
+@pytest.mark.parametrize("mode", ["mask", "check"])
+def test_stencil_out_crossing_end(arenas, mode):
+    """out's last rows lie past end: mask wraps them to the
+    start of the partition (kept free), check drops them and counts."""
+    a, parts, rng = _setup(arenas, seed=12)
+    H, W, pitch = 200, 1000, 1024
+    p = parts[2]
+    inp = 4 * MiB
+    upload(p.base + inp, synth.uniform_f32(rng, H * pitch, 0.0, 1.0))
+    out = p.end - (H - 9) * pitch * 4
+    _run(a, parts, 2, mode,
+         lambda p: a.stencil(p.id, mode, out, p.base + inp, H, W, pitch, 0.5, 0.125),
+         lambda m, p: oracle.stencil(m, p.base, p.size, mode, out, p.base + inp, H, W, pitch, 0.5, 0.125),
+         None if mode == "mask" else 8 * (W - 2))
+
+
+@pytest.mark.parametrize("mode", ["mask", "check"])
+def test_stencil_in_from_victim(arenas, mode):
+    a, parts, rng = _setup(arenas, seed=13)
+    H, W, pitch = 100, 777, 780
+    p = parts[1]
+    inp = parts[0].base + 2 * MiB                  # someone else's memory
+    upload(parts[0].base + 2 * MiB, synth.uniform_f32(rng, H * pitch))    # finite (NaN-free) in both
+    upload(p.base + 2 * MiB, synth.uniform_f32(rng, H * pitch))           # the victim and the wrap target
+    _run(a, parts, 1, mode,
+         lambda p: a.stencil(p.id, mode, p.base + 8 * MiB, inp, H, W, pitch, 0.5, 0.125),
+         lambda m, p: oracle.stencil(m, p.base, p.size, mode, p.base + 8 * MiB, inp, H, W, pitch, 0.5, 0.125),
+         None if mode == "mask" else 5 * (H - 2) * (W - 2))
+
+
+# ---------------------------------------------------------------------------
+# C1 toy (BASELINE.json configs[0]) on a 1 MiB VMM arena
+# ---------------------------------------------------------------------------
+
+def _toy_upload(a, parts, toy):
+    host = np.zeros(a.size, np.uint8)
+    for t, p in enumerate(parts):
+        o = p.base - a.base
+        host[o + synth.C1_TABLE_OFF:o + synth.C1_TABLE_OFF + 4 * synth.C1_TABLE_N] = toy.tables[t].view(np.uint8)
+        host[o + synth.C1_IDX_OFF:o + synth.C1_IDX_OFF + 4 * synth.C1_N] = toy.idx[t].view(np.uint8)
+    upload(a.base, host)
+    return host
+
+
+@pytest.mark.parametrize("mode", ["mask", "check"])
+def test_c1_toy(arenas, mode):
+    a = arenas(synth.C1_ARENA)
+    parts = [a.partition_alloc(synth.C1_PART) for _ in range(synth.C1_TENANTS)]
+    assert [p.base - a.base for p in parts] == [t * synth.C1_PART for t in range(4)]     # P13 placement
+    toy = synth.toy_gather()
+    host = _toy_upload(a, parts, toy)
+    mem = oracle.Mem(a.base, buf=host.copy())
+    a.stats_reset()
+    total = 0
+    for p in parts:
+        a.gather(p.id, mode, p.base + synth.C1_OUT_OFF, p.base + synth.C1_TABLE_OFF, p.base + synth.C1_IDX_OFF,
+                 synth.C1_N)
+        total += oracle.gather(mem, p.base, p.size, mode, p.base + synth.C1_OUT_OFF, p.base + synth.C1_TABLE_OFF,
+                               p.base + synth.C1_IDX_OFF, synth.C1_N).violations
+    got = download(a.base, a.size)
+    assert np.array_equal(got, mem.buf), first_diff(got, mem.buf)
+    st = a.stats()
+    assert st["violations"] == total == (655 if mode == "check" else 0)
+
+
+def test_c1_unfenced_neighbours_read_victims(arenas):
+    """Native (unfenced) kernel with only neighbour-class OOB indices (raw
+    addresses inside the arena, so nothing faults): it reads other tenants'
+    tables -- the attack the fence prevents."""
+    a = arenas(synth.C1_ARENA)
+    parts = [a.partition_alloc(synth.C1_PART) for _ in range(synth.C1_TENANTS)]
+    toy = synth.toy_gather()
+    for t in range(4):                           # keep only in-bounds + neighbour indices
+        far = (toy.oob_class[t] == 2) | (toy.oob_class[t] == 3)
+        toy.idx[t][far] = 0
+    host = _toy_upload(a, parts, toy)
+    mem = oracle.Mem(a.base, buf=host.copy())
+    for p in parts:
+        a.gather(p.id, "none", p.base + synth.C1_OUT_OFF, p.base, p.base + synth.C1_IDX_OFF, synth.C1_N)
+        c = oracle.gather(mem, a.base, a.size, "none", p.base + synth.C1_OUT_OFF, p.base, p.base + synth.C1_IDX_OFF,
+                          synth.C1_N)
+        assert c.faults == 0
+    got = download(a.base, a.size)
+    assert np.array_equal(got, mem.buf), first_diff(got, mem.buf)
+    # and at least one value really came from a victim's table
+    t = 1
+    nb = toy.oob_class[t] == 1
+    out = got[parts[t].base - a.base + synth.C1_OUT_OFF:][:4 * synth.C1_N].view(np.uint32)
+    words = host.view(np.uint32)
+    j = toy.idx[t].astype(np.int64)[nb]
+    np.testing.assert_array_equal(out[nb], words[t * 65536 + j])
+
+
+def test_c1_chaos_mask_race_exposed_excluded(arenas):
+    """Any int32 index (incl. INT32_MAX, -1): mask mode may wrap a read onto
+    `out`, which the same launch writes (race-exposed).
+    Those elements are excluded -- their number is deterministic and reported
+    -- everything else must match the oracle exactly; check mode is fully exact."""
+    a = arenas(synth.C1_ARENA)
+    parts = [a.partition_alloc(synth.C1_PART) for _ in range(synth.C1_TENANTS)]
+    rng = synth.rng_for(1099)
+    toy = synth.toy_gather()
+    for t in range(4):
+        toy.idx[t] = synth.chaos_indices(rng, synth.C1_N)
+    for mode in ("mask", "check"):
+        host = _toy_upload(a, parts, toy)
+        mem = oracle.Mem(a.base, buf=host.copy())
+        excluded = np.zeros(a.size, bool)
+        for t, p in enumerate(parts):
+            out = p.base + synth.C1_OUT_OFF
+            a.gather(p.id, mode, out, p.base, p.base + synth.C1_IDX_OFF, synth.C1_N)
+            oracle.gather(mem, p.base, p.size, mode, out, p.base, p.base + synth.C1_IDX_OFF, synth.C1_N)
+            if mode == "mask":
+                for i, jj in enumerate(toy.idx[t].astype(np.int64)):
+                    r, ok = oracle.resolve(p.base, p.size, "mask", (p.base + 4 * int(jj)) % 2**64, 4)
+                    if out <= r < out + 4 * synth.C1_N:
+                        o = out - a.base + 4 * i
+                        excluded[o:o + 4] = True
+        got = download(a.base, a.size)
+        keep = ~excluded
+        assert np.array_equal(got[keep], mem.buf[keep]), first_diff(got[keep], mem.buf[keep])
+        if mode == "mask":
+            n_ex = int(excluded.sum()) // 4
+            print(f"chaos suite: {n_ex} race-exposed elements excluded")
+            assert n_ex >= 4                       # -1 and INT32_MAX wrap onto out, per tenant

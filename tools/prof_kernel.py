@@ -1,0 +1,51 @@
+"""Launch one fenced kernel a few times on a single tenant partition (for ncu).
+
+  python tools/prof_kernel.py --kind saxpy --mode mask [--reps 3]
+Sizes are the bench's per-tenant sizes (4 GiB tensors; C3 gather; 8192^3 GEMM;
+32768^2 stencil) in a 16 GiB partition.
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2401_09290_b200 import devmem, guardian as g  # noqa: E402
+
+GiB = 1 << 30
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kind", default="saxpy")
+    ap.add_argument("--mode", default="mask")
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    ar = g.Arena(0, 1 << 34)
+    p = ar.partition_alloc(1 << 34)
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(2000)
+    b = p.base
+    for _ in range(a.reps):
+        if a.kind == "copy":
+            ar.copy(p.id, a.mode, b + 4 * GiB, b, 4 * GiB)
+        elif a.kind == "saxpy":
+            ar.saxpy(p.id, a.mode, 1.5, b + 8 * GiB, b + 12 * GiB, 1 << 30)
+        elif a.kind == "gather":
+            ar.gather(p.id, a.mode, b + 2 * GiB + GiB // 4, b, b + 2 * GiB, 1 << 26)
+        elif a.kind == "scatter":
+            ar.scatter(p.id, a.mode, b, b + 2 * GiB, b + 2 * GiB + GiB // 4, 1 << 26)
+        elif a.kind == "stencil":
+            ar.stencil(p.id, a.mode, b + 8 * GiB, b + 4 * GiB, 32768, 32768, 32768, 0.5, 0.125)
+        elif a.kind == "gemm":
+            n = 8192
+            ar.gemm(p.id, a.mode, b + 2 * n * n * 2, b, b + n * n * 2, n, n, n, n, n, n)
+    torch.cuda.synchronize()
+    print("flags", ar.device_flags())
+    ar.close()
+
+
+if __name__ == "__main__":
+    main()
