@@ -316,8 +316,10 @@ def run_gpu(args):
                "steps": args.e2e_steps, "note": "pinned host buffers, checked gd_memcpy_h2d/d2h, PCIe-bound"}
 
     # ---- statistics reduced over GPUs with NCCL (the one collective) ----
-    st = w.arena.stats()
-    red = allreduce([float(st["violations"]), float(st["launches"]), float(st["bytes"])], op="sum")
+    from paper_2401_09290_b200 import dist as gdist
+    per = {rank * TENANTS + t: w.arena.stats(p.id) for t, p in enumerate(w.parts)}
+    red_t, span = gdist.allreduce_stats(per, ms, world * TENANTS)
+    red = [sum(d[f] for d in red_t.values()) for f in ("violations", "launches", "bytes")]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

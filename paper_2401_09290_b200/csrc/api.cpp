@@ -441,7 +441,6 @@ gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry)
     uint64_t base, size;
     gd_status st = snapshot(a, w.tenant, &base, &size);
     if (st != GD_OK) return st;
-    if (a->device < 0) return GD_ERR_UNSUPPORTED;
 
     uint64_t bytes = 0, flops = 0, t;
     bool empty = false;
@@ -494,6 +493,7 @@ gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry)
         }
     }
     if (dry || empty) return GD_OK;
+    if (a->device < 0) return GD_ERR_UNSUPPORTED;      // virtual arena: bookkeeping only
 
     FenceDesc fd;
     fd.base = base;

@@ -1,0 +1,175 @@
+"""Per-kernel throughput at the BASELINE.json sizes, fenced vs unfenced.
+
+For every kernel (C2 copy/saxpy, C3 gather/scatter at 0/1/10 % OOB, C4 stencil
+32768^2 and GEMM 8192^3) the three modes are timed interleaved (none, mask,
+check) with CUDA events on the launching stream, R repetitions after warm-up;
+reports the median, the paper-style mean of 10 without min/max,
+GB/s (TFLOP/s), fraction of the measured peak and overhead vs the unfenced
+twin.  Check-mode violation counts are verified against the planted counts.
+
+  python tools/kernel_bench.py [--reps 12] [--only gather,gemm] > out.json
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2401_09290_b200 import devmem, guardian as g  # noqa: E402
+
+GiB = 1 << 30
+PART = 1 << 34
+
+
+def peaks():
+    d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    return d["hbm_gbs"], d["bf16_tflops"], d["bf16_tflops_sustained"]
+
+
+def paper_mean(xs):
+    xs = sorted(xs)
+    core = xs[1:-1] if len(xs) > 2 else xs
+    return statistics.mean(core)
+
+
+def time_modes(launch, reps, warm=3):
+    """launch(mode, stream) -> None; interleaved none/mask/check."""
+    s = torch.cuda.Stream()
+    res = {m: [] for m in ("none", "mask", "check")}
+    with torch.cuda.stream(s):
+        for m in res:
+            for _ in range(warm):
+                launch(m, s)
+        for _ in range(reps):
+            for m in res:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                launch(m, s)
+                b.record(s)
+                b.synchronize()
+                res[m].append(a.elapsed_time(b))
+    return res
+
+
+def summarize(name, res, work, unit, peak):
+    out = {}
+    for m, xs in res.items():
+        med = statistics.median(xs)
+        rate = work / (med / 1e3) / (1e9 if unit == "GB/s" else 1e12)
+        out[m] = {"ms_median": round(med, 4), "ms_paper_mean": round(paper_mean(xs), 4), unit: round(rate, 1),
+                  "frac_of_peak": round(rate / peak, 4)}
+    for m in ("mask", "check"):
+        out[m]["overhead_pct"] = round(100 * (out[m]["ms_median"] / out["none"]["ms_median"] - 1), 2)
+    print(f"{name:28s} " + "  ".join(f"{m}: {out[m][unit]:8.1f} {unit}" + (f" ({out[m]['overhead_pct']:+.2f}%)"
+                                                                           if m != 'none' else '')
+                                     for m in out), file=sys.stderr)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=12)
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    only = set(args.only.split(",")) if args.only else None
+    hbm, bf16, bf16s = peaks()
+    torch.cuda.set_device(0)
+    arena = g.Arena(0, 2 * PART)
+    victim = arena.partition_alloc(PART)
+    p = arena.partition_alloc(PART)
+    b = p.base
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(2001)
+    results = {"peaks": {"hbm_gbs": hbm, "bf16_tflops": bf16, "bf16_tflops_sustained": bf16s},
+               "device": torch.cuda.get_device_name(0)}
+
+    def want(k):
+        return only is None or k in only
+
+    if want("copy") or want("saxpy"):
+        devmem.view(b, GiB, torch.int32).random_(generator=gen)
+        devmem.view(b + 8 * GiB, 1 << 30, torch.float32).uniform_(-1, 1, generator=gen)
+        devmem.view(b + 12 * GiB, 1 << 30, torch.float32).uniform_(-1, 1, generator=gen)
+    if want("copy"):
+        r = time_modes(lambda m, s: arena.copy(p.id, m, b + 4 * GiB, b, 4 * GiB, stream=s), args.reps)
+        results["copy_4GiB"] = summarize("copy 4 GiB", r, 2 * 4 * GiB, "GB/s", hbm)
+    if want("saxpy"):
+        r = time_modes(lambda m, s: arena.saxpy(p.id, m, 1.5, b + 8 * GiB, b + 12 * GiB, 1 << 30, stream=s),
+                       args.reps)
+        results["saxpy_2^30"] = summarize("saxpy 2^30", r, 12 * (1 << 30), "GB/s", hbm)
+
+    if want("gather") or want("scatter"):
+        # C3 layout: table 2^29 u32 @0, idx 2^26 @2 GiB, out/src @2.25 GiB, pattern [2.5 GiB, 16 GiB)
+        n, T = 1 << 26, 1 << 29
+        devmem.view(b, T, torch.int32).random_(generator=gen)
+        devmem.view(b + 2 * GiB + GiB // 4, n, torch.int32).random_(generator=gen)
+        arena.fill(p.id, 1, 2 * GiB + GiB // 2, PART - 2 * GiB - GiB // 2)
+        for frac in (0.0, 0.01, 0.1):
+            rng = synth.rng_for(3000 + int(frac * 100))
+            idx, pos = synth.indices_with_oob(rng, n, T, frac)
+            devmem.view(b + 2 * GiB, n, torch.int32).copy_(torch.from_numpy(idx))
+            torch.cuda.synchronize()
+            if want("gather"):
+                arena.stats_reset()
+                arena.gather(p.id, "check", b + 2 * GiB + GiB // 4, b, b + 2 * GiB, n)
+                v = arena.stats(p.id)["violations"]
+                assert v == len(pos), (v, len(pos))
+                r = time_modes(lambda m, s: arena.gather(p.id, m, b + 2 * GiB + GiB // 4, b, b + 2 * GiB, n, stream=s),
+                               args.reps)
+                res = summarize(f"gather 2^26 oob={frac}", r, 12 * n, "GB/s", hbm)
+                res["violations_check"] = v
+                results[f"gather_oob{frac}"] = res
+            if want("scatter") and frac in (0.0, 0.01):
+                arena.stats_reset()
+                arena.scatter(p.id, "check", b, b + 2 * GiB, b + 2 * GiB + GiB // 4, n)
+                v = arena.stats(p.id)["violations"]
+                assert v == len(pos), (v, len(pos))
+                r = time_modes(lambda m, s: arena.scatter(p.id, m, b, b + 2 * GiB, b + 2 * GiB + GiB // 4, n,
+                                                          stream=s), args.reps)
+                res = summarize(f"scatter 2^26 oob={frac}", r, 16 * n, "GB/s", hbm)
+                res["violations_check"] = v
+                results[f"scatter_oob{frac}"] = res
+
+    if want("stencil"):
+        H = W = 32768
+        devmem.view(b + 4 * GiB, H * W, torch.float32).uniform_(0, 1, generator=gen)
+        r = time_modes(lambda m, s: arena.stencil(p.id, m, b + 8 * GiB, b + 4 * GiB, H, W, W, 0.5, 0.125, stream=s),
+                       args.reps)
+        results["stencil_32768^2"] = summarize("stencil 32768^2", r, 8 * (H - 2) * (W - 2), "GB/s", hbm)
+
+    if want("gemm"):
+        n = 8192
+        A, B, C = b, b + n * n * 2, b + 2 * n * n * 2
+        devmem.view(A, n * n, torch.bfloat16).uniform_(-1, 1, generator=gen)
+        devmem.view(B, n * n, torch.bfloat16).uniform_(-1, 1, generator=gen)
+        r = time_modes(lambda m, s: arena.gemm(p.id, m, C, A, B, n, n, n, n, n, n, stream=s), max(4, args.reps // 2))
+        res = summarize("gemm 8192^3 bf16", r, 2 * n ** 3, "TFLOP/s", bf16)
+        ta = devmem.view(A, n * n, torch.bfloat16).view(n, n)
+        tb = devmem.view(B, n * n, torch.bfloat16).view(n, n)
+        xs = []
+        for i in range(3 + max(4, args.reps // 2)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(ta, tb.t())
+            e1.record()
+            e1.synchronize()
+            if i >= 3:
+                xs.append(e0.elapsed_time(e1))
+        res["torch_matmul"] = {"ms_median": round(statistics.median(xs), 4),
+                               "TFLOP/s": round(2 * n ** 3 / (statistics.median(xs) / 1e3) / 1e12, 1)}
+        print(f"  torch.matmul: {res['torch_matmul']['TFLOP/s']} TFLOP/s", file=sys.stderr)
+        results["gemm_8192^3"] = res
+    results["device_flags"] = arena.device_flags()
+    print(json.dumps(results))
+    arena.close()
+
+
+if __name__ == "__main__":
+    main()

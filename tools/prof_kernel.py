@@ -28,6 +28,13 @@ def main():
     gen = torch.Generator(device="cuda:0")
     gen.manual_seed(2000)
     b = p.base
+    if a.kind in ("gather", "scatter"):
+        # C3: uniform in-bounds indices into the 2^29-entry table, 1 % planted below the base
+        idx = devmem.view(b + 2 * GiB, 1 << 26, torch.int32)
+        idx.random_(0, 1 << 29, generator=gen)
+        pos = torch.randperm(1 << 26, generator=gen, device="cuda:0")[: (1 << 26) // 100]
+        idx[pos] = torch.randint(-2**31, 0, (pos.numel(),), generator=gen, device="cuda:0", dtype=torch.int32)
+        devmem.view(b, 1 << 29, torch.int32).random_(generator=gen)
     for _ in range(a.reps):
         if a.kind == "copy":
             ar.copy(p.id, a.mode, b + 4 * GiB, b, 4 * GiB)
