@@ -41,10 +41,21 @@ struct Fence {
     }
 };
 
+// Check-mode hoisting: true iff every byte of [a, a+len) lies in the
+// partition (no 64-bit wraparound).  A CTA whose whole tile passes this test
+// performs exactly the accesses the per-access check would allow (all of
+// them) and refuses none, so it may run the unchecked body; only tiles that
+// touch or cross the partition edge pay for per-access checks.
+__device__ __forceinline__ bool range_in(const FenceDesc &fd, uint64_t a, uint64_t len) {
+    const uint64_t size = fd.mask + 1, off = a - fd.base;
+    return len <= size && off <= size - len;
+}
+
 // Sum a per-thread refusal count over the CTA and add it to the trusted
 // counter with one atomic per CTA.  All threads of the
 // CTA must call it.
 __device__ __forceinline__ void flush_violations(uint32_t nv_thread, unsigned long long *viol) {
+    if (!__syncthreads_or(nv_thread != 0)) return;    // common case: nothing refused in this CTA
     __shared__ unsigned long long warp_sums[32];
     uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     unsigned long long nv = nv_thread;

@@ -15,14 +15,19 @@
 // Same principle as the per-access fence; sm_86 has no
 // TMA, so the paper has no passage for it (reading R-TMA).
 //
-// Kernel: one 128 x 256 output tile per CTA; warp 0 = TMA producer (one
-// elected thread, 4-stage mbarrier ring of 48 KB stages, 128-byte swizzle),
-// warp 1 = MMA issuer (one thread: tcgen05.mma.cta_group::1.kind::f16,
-// M=128 N=256 K=16, fp32 accumulator in TMEM, 256 columns), warp 2 = TMEM
-// allocator, warps 4-7 = epilogue (tcgen05.ld 32x32b -> bf16 -> st.global,
-// rows clamped to the C extent).  All waits are bounded: a kernel that
-// cannot make progress sets a device error word and exits instead of hanging
-// the shared context.
+// Kernel (persistent, one CTA per SM, 128 x 256 output tiles in a grouped
+// raster so the tiles in flight share A and B panels in L2):
+//   warp 0     TMA producer: one elected thread, 4-stage mbarrier ring of
+//              48 KB stages (A 128x64, B 256x64 bf16, 128-byte swizzle);
+//   warp 1     MMA issuer: one thread, tcgen05.mma.cta_group::1.kind::f16
+//              M=128 N=256 K=16, fp32 accumulators in TMEM, double-buffered
+//              (2 x 256 columns) so the epilogue of tile i overlaps the
+//              mainloop of tile i+1;
+//   warp 2     TMEM allocator (512 columns);
+//   warps 4-7  epilogue: tcgen05.ld 32x32b -> bf16 -> st.global, rows
+//              clamped to the C extent, then release the accumulator.
+// All waits are bounded: a kernel that cannot make progress sets a device
+// error word and exits instead of hanging the shared context.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -34,13 +39,14 @@
 namespace gd {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4, ACC = 2;
 constexpr uint32_t A_BYTES = BM * BK * 2;          // 16 KB
 constexpr uint32_t B_BYTES = BN * BK * 2;          // 32 KB
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int THREADS = 256;
-constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t TMEM_COLS = ACC * BN;           // 512
+constexpr uint32_t GROUP_M = 16;                   // raster group (m-blocks)
 
 // instruction descriptor: D f32, A/B bf16, both K-major, N=256, M=128
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -49,17 +55,31 @@ __device__ unsigned int g_gemm_timeout = 0;        // set if a bounded wait expi
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Wait for the phase of `bar` with parity `parity`; give up after ~2 s (a
+// stalled pipeline is a bug: report it instead of hanging every tenant).
 __device__ __forceinline__ bool mbar_wait(uint32_t bar, uint32_t parity) {
-    for (uint32_t spin = 0; spin < (1u << 26); spin++) {
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0;; spin++) {
         uint32_t done;
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
-            : "r"(bar), "r"(parity), "r"(0x989680u)
+            : "r"(bar), "r"(parity)
             : "memory");
         if (done) return true;
+        if ((spin & 1023u) == 0) {
+            const uint64_t now = globaltimer();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 2000000000ull) break;
+        }
     }
     atomicExch(&g_gemm_timeout, 1u);
     return false;
@@ -72,18 +92,28 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
+// grouped raster: tiles t = 0..tm*tn-1 -> (m_blk, n_blk)
+__device__ __forceinline__ void tile_coords(uint32_t t, uint32_t tm, uint32_t tn, uint32_t &mb, uint32_t &nb) {
+    const uint32_t per_group = GROUP_M * tn;
+    const uint32_t g = t / per_group, first = g * GROUP_M;
+    const uint32_t gm = (tm - first < GROUP_M) ? tm - first : GROUP_M;
+    const uint32_t r = t - g * per_group;
+    mb = first + r % gm;
+    nb = r / gm;
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
 k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, uint64_t C, uint64_t ldc,
-       uint32_t N, uint32_t K, uint64_t rowsC) {
+       uint32_t N, uint32_t K, uint64_t rowsC, uint32_t tm, uint32_t tn) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *bars = (uint64_t *)(smem + STAGES * STAGE_BYTES);
-    uint64_t *full = bars, *empty = bars + STAGES, *tmem_full = bars + 2 * STAGES;
-    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * STAGES + 1);
+    uint64_t *full = bars, *empty = bars + STAGES;
+    uint64_t *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + ACC;
+    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * STAGES + 2 * ACC);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-    const uint32_t nkb = K / BK;
+    const uint32_t nkb = K / BK, ntiles = tm * tn;
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -92,7 +122,10 @@ k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
         }
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(tmem_full)));
+        for (int a = 0; a < ACC; a++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tfull[a])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smem_u32(&tempty[a])));   // 4 epilogue warps
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -107,82 +140,111 @@ k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
-        for (uint32_t kb = 0; kb < nkb; kb++) {
-            const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1;
-            if (!mbar_wait(smem_u32(&empty[s]), ph ^ 1)) break;
-            const uint32_t fb = smem_u32(&full[s]);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(STAGE_BYTES)
-                         : "memory");
-            const uint32_t sa = smem_u32(smem + s * STAGE_BYTES), sb = sa + A_BYTES;
-            const int kc = (int)(kb * BK);
-            asm volatile(
-                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-                ::"r"(sa), "l"(&tmA), "r"(fb), "r"(kc), "r"((int)m0)
-                : "memory");
-            asm volatile(
-                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-                ::"r"(sb), "l"(&tmB), "r"(fb), "r"(kc), "r"((int)n0)
-                : "memory");
+        uint32_t it = 0;
+        bool alive = true;
+        for (uint32_t t = blockIdx.x; t < ntiles && alive; t += gridDim.x) {
+            uint32_t mb, nb;
+            tile_coords(t, tm, tn, mb, nb);
+            for (uint32_t kb = 0; kb < nkb; kb++, it++) {
+                const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+                if (!mbar_wait(smem_u32(&empty[s]), ph ^ 1)) { alive = false; break; }
+                const uint32_t fb = smem_u32(&full[s]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(STAGE_BYTES)
+                             : "memory");
+                const uint32_t sa = smem_u32(smem + s * STAGE_BYTES), sb = sa + A_BYTES;
+                const int kc = (int)(kb * BK);
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                    ::"r"(sa), "l"(&tmA), "r"(fb), "r"(kc), "r"((int)(mb * BM))
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                    ::"r"(sb), "l"(&tmB), "r"(fb), "r"(kc), "r"((int)(nb * BN))
+                    : "memory");
+            }
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer ----------------
-        for (uint32_t kb = 0; kb < nkb; kb++) {
-            const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1;
-            if (!mbar_wait(smem_u32(&full[s]), ph)) break;
+        uint32_t it = 0, tl = 0;
+        bool alive = true;
+        for (uint32_t t = blockIdx.x; t < ntiles && alive; t += gridDim.x, tl++) {
+            const uint32_t acc = tl & 1, aph = (tl >> 1) & 1;
+            if (!mbar_wait(smem_u32(&tempty[acc]), aph ^ 1)) break;     // epilogue drained this accumulator
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t sa = smem_u32(smem + s * STAGE_BYTES), sb = sa + A_BYTES;
+            const uint32_t dacc = tmem + acc * BN;
+            for (uint32_t kb = 0; kb < nkb; kb++, it++) {
+                const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+                if (!mbar_wait(smem_u32(&full[s]), ph)) { alive = false; break; }
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t sa = smem_u32(smem + s * STAGE_BYTES), sb = sa + A_BYTES;
 #pragma unroll
-            for (int k = 0; k < BK / 16; k++) {
-                const uint64_t da = sw128_desc(sa + 32 * k), db = sw128_desc(sb + 32 * k);
-                const uint32_t acc = (kb | k) ? 1u : 0u;
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-                    ::"r"(tmem), "l"(da), "l"(db), "r"(IDESC), "r"(acc)
-                    : "memory");
+                for (int k = 0; k < BK / 16; k++) {
+                    const uint64_t da = sw128_desc(sa + 32 * k), db = sw128_desc(sb + 32 * k);
+                    const uint32_t accum = (kb | k) ? 1u : 0u;
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                        ::"r"(dacc), "l"(da), "l"(db), "r"(IDESC), "r"(accum)
+                        : "memory");
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                             ::"r"(smem_u32(&empty[s]))
+                             : "memory");
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                         ::"r"(smem_u32(&empty[s]))
+                         ::"r"(smem_u32(&tfull[acc]))
                          : "memory");
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                     ::"r"(smem_u32(tmem_full))
-                     : "memory");
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> registers -> bf16 -> global ----------------
         const uint32_t wq = warp - 4;                  // TMEM lanes 32*wq .. 32*wq+31
-        const bool ok = mbar_wait(smem_u32(tmem_full), 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t row = (uint64_t)m0 + wq * 32 + lane;
-        const bool store_row = ok && row < rowsC;
+        uint32_t tl = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, tl++) {
+            uint32_t mb, nb;
+            tile_coords(t, tm, tn, mb, nb);
+            const uint32_t acc = tl & 1, aph = (tl >> 1) & 1;
+            if (!mbar_wait(smem_u32(&tfull[acc]), aph)) break;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t row = (uint64_t)mb * BM + wq * 32 + lane;
+            const bool store_row = row < rowsC;
+            const uint32_t n0 = nb * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; c++) {
-            uint32_t v[32];
-            const uint32_t taddr = tmem + ((wq * 32u) << 16) + (uint32_t)(c * 32);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (store_row) {
+            for (int c = 0; c < BN / 32; c++) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((wq * 32u) << 16) + acc * BN + (uint32_t)(c * 32);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c == BN / 32 - 1) {
+                    // accumulator fully read: hand it back to the MMA warp
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc]))
+                                     : "memory");
+                }
+                if (store_row) {
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const uint32_t col = n0 + c * 32 + q * 8;
-                    if (col < N) {
-                        uint32_t p[4];
+                    for (int q = 0; q < 4; q++) {
+                        const uint32_t col = n0 + c * 32 + q * 8;
+                        if (col < N) {
+                            uint32_t p[4];
 #pragma unroll
-                        for (int e = 0; e < 4; e++) {
-                            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * e]),
-                                                                     __uint_as_float(v[q * 8 + 2 * e + 1]));
-                            p[e] = *reinterpret_cast<uint32_t *>(&h);
+                            for (int e = 0; e < 4; e++) {
+                                __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * e]),
+                                                                         __uint_as_float(v[q * 8 + 2 * e + 1]));
+                                p[e] = *reinterpret_cast<uint32_t *>(&h);
+                            }
+                            uint4 *dst = reinterpret_cast<uint4 *>(C + 2 * (row * ldc + col));
+                            *dst = make_uint4(p[0], p[1], p[2], p[3]);
                         }
-                        uint4 *dst = reinterpret_cast<uint4 *>(C + 2 * (row * ldc + col));
-                        *dst = make_uint4(p[0], p[1], p[2], p[3]);
                     }
                 }
             }
@@ -233,7 +295,7 @@ uint64_t desc_rows(int mode, uint64_t base, uint64_t size, uint64_t p, uint64_t 
 }
 
 gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t size, cudaStream_t s,
-                        const Geom &) {
+                        const Geom &g) {
     const uint32_t M = w.u32[0], N = w.u32[1], K = w.u32[2];
     const uint64_t lda = w.u64[0], ldb = w.u64[1], ldc = w.u64[2];
     uint64_t Af, Bf, Cf;
@@ -249,6 +311,7 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
         }
     }
     if (rC == 0) return GD_OK;                         // nothing may be stored
+    uint64_t ldA = lda, ldB = ldb;
     if (rA == 0 || rB == 0) {
         // an operand with no rows reads as zeros: point its map at a trusted
         // zero row outside every partition
@@ -263,21 +326,21 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
             if (e != cudaSuccess) return cuda_status(e);
             a->zero_bytes = 2ull * K;
         }
-        if (rA == 0) { Af = (uint64_t)a->zero_buf; rA = 1; }
-        if (rB == 0) { Bf = (uint64_t)a->zero_buf; rB = 1; }
+        if (rA == 0) { Af = (uint64_t)a->zero_buf; rA = 1; ldA = K; }
+        if (rB == 0) { Bf = (uint64_t)a->zero_buf; rB = 1; ldB = K; }
     }
     CUtensorMap tmA, tmB;
     std::memset(&tmA, 0, sizeof(tmA));
     std::memset(&tmB, 0, sizeof(tmB));
-    const uint64_t ldA = (Af == (uint64_t)a->zero_buf) ? K : lda, ldB = (Bf == (uint64_t)a->zero_buf) ? K : ldb;
     if (!make_map(&tmA, Af, K, rA, ldA, BM) || !make_map(&tmB, Bf, K, rB, ldB, BN)) return GD_ERR_UNSUPPORTED;
     static bool attr = [] {
         return cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) == cudaSuccess;
     }();
     if (!attr) return cuda_status(cudaErrorInvalidValue);
-    const uint32_t rows = (uint32_t)rC;                // rC <= M
-    const dim3 grid((N + BN - 1) / BN, (rows + BM - 1) / BM);
-    k_gemm<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, Cf, ldc, N, K, rC);
+    const uint32_t tm = (uint32_t)((rC + BM - 1) / BM), tn = (N + BN - 1) / BN;   // rC <= M
+    const uint32_t ntiles = tm * tn;
+    const uint32_t grid = ntiles < (uint32_t)g.sms ? ntiles : (uint32_t)g.sms;
+    k_gemm<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, Cf, ldc, N, K, rC, tm, tn);
     return cuda_status(cudaGetLastError());
 }
 

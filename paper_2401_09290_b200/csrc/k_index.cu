@@ -6,10 +6,13 @@
 // PAPER.md:206-209) and only then fenced (second addressing
 // mode) -- the fence never sees a partial address.
 //
-// D = 1 path: 128-bit index loads, 4 independent fenced random 32-bit table
-// loads per index vector, x2 unrolled (8 random loads in flight per thread),
-// 128-bit output stores.  D > 1 path: one warp per index row, lanes stride
-// over the row; lane 0 loads the index once (one logical access, as in the
+// D = 1 path: each CTA owns a contiguous chunk of kThreads x kU index
+// vectors; per thread kU 128-bit index loads, then 4 kU independent fenced
+// random 32-bit table loads (L1-bypassing, sector-granular), then kU 128-bit
+// output stores.  In check mode the index and output streams are range-tested
+// once per CTA chunk (fence.cuh range_in); the random table accesses are
+// checked one by one.  D > 1 path: one warp per index row, lanes stride over
+// the row; lane 0 loads the index once (one logical access, as in the
 // oracle) and broadcasts it.
 #include "fence.cuh"
 #include "kernels.h"
@@ -18,11 +21,12 @@ namespace gd {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 2;
+constexpr int kU = 4;
+constexpr uint64_t kChunk = (uint64_t)kThreads * kU;   // index vectors per CTA
 
 __device__ __forceinline__ int4 ld_idx(uint64_t a) { return __ldcs(reinterpret_cast<const int4 *>(a)); }
 __device__ __forceinline__ uint4 ld_u4(uint64_t a) { return __ldcs(reinterpret_cast<const uint4 *>(a)); }
-__device__ __forceinline__ uint32_t ld_tab(uint64_t a) { return __ldg(reinterpret_cast<const uint32_t *>(a)); }
+__device__ __forceinline__ uint32_t ld_tab(uint64_t a) { return __ldcg(reinterpret_cast<const uint32_t *>(a)); }
 __device__ __forceinline__ void st_out(uint64_t a, uint4 v) { __stcs(reinterpret_cast<uint4 *>(a), v); }
 
 __device__ __forceinline__ uint64_t row_addr(uint64_t table, int32_t j) {
@@ -37,58 +41,68 @@ __device__ __forceinline__ uint32_t fenced_tab(const Fence<MODE, 4> &f4, uint64_
     return 0u;
 }
 
+__device__ __forceinline__ uint64_t chunk_len(uint64_t nvec, uint64_t c0) {
+    return nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
+}
+
 // ---------------------------------------------------------------------------
 // K3, D = 1: out[i] = table[sext(idx[i])]
+// SMODE fences the index/output streams, TMODE the table accesses.
 // ---------------------------------------------------------------------------
-template <int MODE>
-__global__ void __launch_bounds__(kThreads, 4) k_gather1(const __grid_constant__ FenceDesc fd, uint64_t out,
-                                                      uint64_t table, uint64_t idx, uint64_t nvec,
-                                                      uint32_t tail) {
-    const Fence<MODE, 16> f16(fd);
-    const Fence<MODE, 4> f4(fd);
-    uint32_t nv = 0;
-    const uint64_t T = (uint64_t)gridDim.x * kThreads;
-    uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    for (; v + (kUnroll - 1) * T < nvec; v += kUnroll * T) {
-        int4 j[kUnroll];
+template <int SMODE, int TMODE>
+__device__ __forceinline__ void gather_chunk(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t idx,
+                                             uint64_t v0, uint64_t nvec, uint32_t &nv) {
+    const Fence<SMODE, 16> f16(fd);
+    const Fence<TMODE, 4> f4(fd);
+    int4 j[kU];
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-            const uint64_t a = idx + 16 * (v + u * T);
-            j[u] = make_int4(0, 0, 0, 0);
+    for (int u = 0; u < kU; u++) {
+        const uint64_t v = v0 + u * kThreads;
+        j[u] = make_int4(0, 0, 0, 0);
+        if (v < nvec) {
+            const uint64_t a = idx + 16 * v;
             if (f16.ok(a)) j[u] = ld_idx(f16.addr(a));
             else nv += 4;
         }
-        uint4 r[kUnroll];
+    }
+    uint4 r[kU];
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-            r[u].x = fenced_tab<MODE>(f4, table, j[u].x, nv);
-            r[u].y = fenced_tab<MODE>(f4, table, j[u].y, nv);
-            r[u].z = fenced_tab<MODE>(f4, table, j[u].z, nv);
-            r[u].w = fenced_tab<MODE>(f4, table, j[u].w, nv);
+    for (int u = 0; u < kU; u++) {
+        if (v0 + u * kThreads < nvec) {
+            r[u].x = fenced_tab<TMODE>(f4, table, j[u].x, nv);
+            r[u].y = fenced_tab<TMODE>(f4, table, j[u].y, nv);
+            r[u].z = fenced_tab<TMODE>(f4, table, j[u].z, nv);
+            r[u].w = fenced_tab<TMODE>(f4, table, j[u].w, nv);
         }
+    }
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-            const uint64_t a = out + 16 * (v + u * T);
+    for (int u = 0; u < kU; u++) {
+        const uint64_t v = v0 + u * kThreads;
+        if (v < nvec) {
+            const uint64_t a = out + 16 * v;
             if (f16.ok(a)) st_out(f16.addr(a), r[u]);
             else nv += 4;
         }
     }
-    for (; v < nvec; v += T) {
-        const uint64_t ai = idx + 16 * v, ao = out + 16 * v;
-        int4 j = make_int4(0, 0, 0, 0);
-        if (f16.ok(ai)) j = ld_idx(f16.addr(ai));
-        else nv += 4;
-        uint4 r;
-        r.x = fenced_tab<MODE>(f4, table, j.x, nv);
-        r.y = fenced_tab<MODE>(f4, table, j.y, nv);
-        r.z = fenced_tab<MODE>(f4, table, j.z, nv);
-        r.w = fenced_tab<MODE>(f4, table, j.w, nv);
-        if (f16.ok(ao)) st_out(f16.addr(ao), r);
-        else nv += 4;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_gather1(const __grid_constant__ FenceDesc fd, uint64_t out,
+                                                      uint64_t table, uint64_t idx, uint64_t nvec, uint32_t tail) {
+    uint32_t nv = 0;
+    const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, v0 = c0 + threadIdx.x;
+    if constexpr (MODE == kCheck) {
+        const uint64_t cn = chunk_len(nvec, c0);
+        if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, out + 16 * c0, 16 * cn))
+            gather_chunk<kNone, kCheck>(fd, out, table, idx, v0, nvec, nv);
+        else
+            gather_chunk<kCheck, kCheck>(fd, out, table, idx, v0, nvec, nv);
+    } else {
+        gather_chunk<MODE, MODE>(fd, out, table, idx, v0, nvec, nv);
     }
-    const uint64_t tid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (tid < tail) {
-        const uint64_t ai = idx + 16 * nvec + 4 * tid, ao = out + 16 * nvec + 4 * tid;
+    if (blockIdx.x == 0 && threadIdx.x < tail) {
+        const Fence<MODE, 4> f4(fd);
+        const uint64_t ai = idx + 16 * nvec + 4 * threadIdx.x, ao = out + 16 * nvec + 4 * threadIdx.x;
         int32_t j = 0;
         if (f4.ok(ai)) j = *reinterpret_cast<const int32_t *>(f4.addr(ai));
         else nv++;
@@ -144,51 +158,54 @@ __device__ __forceinline__ void fenced_red(const Fence<MODE, 4> &f4, uint64_t ta
     else nv++;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ FenceDesc fd, uint64_t table,
-                                                      uint64_t idx, uint64_t src, uint64_t nvec, uint32_t tail) {
-    const Fence<MODE, 16> f16(fd);
-    const Fence<MODE, 4> f4(fd);
-    uint32_t nv = 0;
-    const uint64_t T = (uint64_t)gridDim.x * kThreads;
-    uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    for (; v + (kUnroll - 1) * T < nvec; v += kUnroll * T) {
-        int4 j[kUnroll];
-        uint4 s[kUnroll];
+template <int SMODE, int TMODE>
+__device__ __forceinline__ void scatter_chunk(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src,
+                                              uint64_t v0, uint64_t nvec, uint32_t &nv) {
+    const Fence<SMODE, 16> f16(fd);
+    const Fence<TMODE, 4> f4(fd);
+    int4 j[kU];
+    uint4 s[kU];
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-            const uint64_t ai = idx + 16 * (v + u * T), as = src + 16 * (v + u * T);
-            j[u] = make_int4(0, 0, 0, 0);
-            s[u] = make_uint4(0, 0, 0, 0);
+    for (int u = 0; u < kU; u++) {
+        const uint64_t v = v0 + u * kThreads;
+        j[u] = make_int4(0, 0, 0, 0);
+        s[u] = make_uint4(0, 0, 0, 0);
+        if (v < nvec) {
+            const uint64_t ai = idx + 16 * v, as = src + 16 * v;
             if (f16.ok(ai)) j[u] = ld_idx(f16.addr(ai));
             else nv += 4;
             if (f16.ok(as)) s[u] = ld_u4(f16.addr(as));
             else nv += 4;
         }
+    }
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-            fenced_red<MODE>(f4, table, j[u].x, s[u].x, nv);
-            fenced_red<MODE>(f4, table, j[u].y, s[u].y, nv);
-            fenced_red<MODE>(f4, table, j[u].z, s[u].z, nv);
-            fenced_red<MODE>(f4, table, j[u].w, s[u].w, nv);
+    for (int u = 0; u < kU; u++) {
+        if (v0 + u * kThreads < nvec) {
+            fenced_red<TMODE>(f4, table, j[u].x, s[u].x, nv);
+            fenced_red<TMODE>(f4, table, j[u].y, s[u].y, nv);
+            fenced_red<TMODE>(f4, table, j[u].z, s[u].z, nv);
+            fenced_red<TMODE>(f4, table, j[u].w, s[u].w, nv);
         }
     }
-    for (; v < nvec; v += T) {
-        const uint64_t ai = idx + 16 * v, as = src + 16 * v;
-        int4 j = make_int4(0, 0, 0, 0);
-        uint4 s = make_uint4(0, 0, 0, 0);
-        if (f16.ok(ai)) j = ld_idx(f16.addr(ai));
-        else nv += 4;
-        if (f16.ok(as)) s = ld_u4(f16.addr(as));
-        else nv += 4;
-        fenced_red<MODE>(f4, table, j.x, s.x, nv);
-        fenced_red<MODE>(f4, table, j.y, s.y, nv);
-        fenced_red<MODE>(f4, table, j.z, s.z, nv);
-        fenced_red<MODE>(f4, table, j.w, s.w, nv);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ FenceDesc fd, uint64_t table,
+                                                      uint64_t idx, uint64_t src, uint64_t nvec, uint32_t tail) {
+    uint32_t nv = 0;
+    const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, v0 = c0 + threadIdx.x;
+    if constexpr (MODE == kCheck) {
+        const uint64_t cn = chunk_len(nvec, c0);
+        if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, src + 16 * c0, 16 * cn))
+            scatter_chunk<kNone, kCheck>(fd, table, idx, src, v0, nvec, nv);
+        else
+            scatter_chunk<kCheck, kCheck>(fd, table, idx, src, v0, nvec, nv);
+    } else {
+        scatter_chunk<MODE, MODE>(fd, table, idx, src, v0, nvec, nv);
     }
-    const uint64_t tid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (tid < tail) {
-        const uint64_t ai = idx + 16 * nvec + 4 * tid, as = src + 16 * nvec + 4 * tid;
+    if (blockIdx.x == 0 && threadIdx.x < tail) {
+        const Fence<MODE, 4> f4(fd);
+        const uint64_t ai = idx + 16 * nvec + 4 * threadIdx.x, as = src + 16 * nvec + 4 * threadIdx.x;
         int32_t j = 0;
         uint32_t s = 0;
         if (f4.ok(ai)) j = *reinterpret_cast<const int32_t *>(f4.addr(ai));
@@ -207,35 +224,27 @@ int blocks_per_sm(K kernel) {
     return b;
 }
 
-uint64_t grid_for(uint64_t threads_wanted, int sms, int bps) {
-    uint64_t want = (threads_wanted + kThreads - 1) / kThreads;
-    const uint64_t cap = (uint64_t)sms * (uint64_t)bps;
-    if (want > cap) want = cap;
-    return want ? want : 1;
+unsigned chunk_grid(uint64_t nvec) {
+    const uint64_t g = (nvec + kChunk - 1) / kChunk;
+    return (unsigned)(g ? g : 1);
 }
 
 template <int MODE>
 cudaError_t gather_t(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t idx, uint64_t n, uint32_t D,
                      cudaStream_t s, const Geom &g) {
     if (D == 1) {
-        static const int bps = blocks_per_sm(k_gather1<MODE>);
-        const uint64_t nvec = n / 4;
-        k_gather1<MODE><<<(unsigned)grid_for(nvec / kUnroll + 1, g.sms, bps), kThreads, 0, s>>>(
-            fd, out, table, idx, nvec, (uint32_t)(n % 4));
+        k_gather1<MODE><<<chunk_grid(n / 4), kThreads, 0, s>>>(fd, out, table, idx, n / 4, (uint32_t)(n % 4));
     } else {
         static const int bps = blocks_per_sm(k_gatherD<MODE>);
-        k_gatherD<MODE><<<(unsigned)grid_for(n * 32, g.sms, bps), kThreads, 0, s>>>(fd, out, table, idx, n, D);
+        const uint64_t want = (n * 32 + kThreads - 1) / kThreads, cap = (uint64_t)g.sms * bps;
+        k_gatherD<MODE><<<(unsigned)(want < cap ? want : cap), kThreads, 0, s>>>(fd, out, table, idx, n, D);
     }
     return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t scatter_t(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src, uint64_t n, cudaStream_t s,
-                      const Geom &g) {
-    static const int bps = blocks_per_sm(k_scatter<MODE>);
-    const uint64_t nvec = n / 4;
-    k_scatter<MODE><<<(unsigned)grid_for(nvec / kUnroll + 1, g.sms, bps), kThreads, 0, s>>>(fd, table, idx, src,
-                                                                                           nvec, (uint32_t)(n % 4));
+cudaError_t scatter_t(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src, uint64_t n, cudaStream_t s) {
+    k_scatter<MODE><<<chunk_grid(n / 4), kThreads, 0, s>>>(fd, table, idx, src, n / 4, (uint32_t)(n % 4));
     return cudaGetLastError();
 }
 
@@ -251,11 +260,11 @@ cudaError_t launch_gather(int mode, const FenceDesc &fd, uint64_t out, uint64_t 
 }
 
 cudaError_t launch_scatter(int mode, const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src, uint64_t n,
-                           cudaStream_t s, const Geom &g) {
+                           cudaStream_t s, const Geom &) {
     switch (mode) {
-        case kNone: return scatter_t<kNone>(fd, table, idx, src, n, s, g);
-        case kMask: return scatter_t<kMask>(fd, table, idx, src, n, s, g);
-        default: return scatter_t<kCheck>(fd, table, idx, src, n, s, g);
+        case kNone: return scatter_t<kNone>(fd, table, idx, src, n, s);
+        case kMask: return scatter_t<kMask>(fd, table, idx, src, n, s);
+        default: return scatter_t<kCheck>(fd, table, idx, src, n, s);
     }
 }
 

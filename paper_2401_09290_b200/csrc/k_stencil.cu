@@ -21,11 +21,10 @@ namespace gd {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kRows = 64;     // rows per CTA strip
-constexpr int kG = 4;         // rows loaded per step
+constexpr int kRows = 64;     // rows per CTA strip (a multiple of the rows loaded per step)
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_stencil(const __grid_constant__ FenceDesc fd, uint64_t out,
+template <int MODE, int kG = (MODE == kCheck ? 2 : 4)>
+__global__ void __launch_bounds__(kThreads, MODE == kCheck ? 3 : 4) k_stencil(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                       uint64_t in, uint32_t H, uint32_t W, uint64_t pitch, float c0,
                                                       float c1) {
     const Fence<MODE, 16> f16(fd);
@@ -41,6 +40,14 @@ __global__ void __launch_bounds__(kThreads) k_stencil(const __grid_constant__ Fe
         for (int k = 0; k < 4; k++) {
             interior[k] = (c + k >= 1) && (c + k + 2 <= W);
             all4 = all4 && interior[k];
+        }
+        // refused-access weights (check mode): loads of the own vector used by
+        // the interior points as C (each), as W (k >= 1) and as E (k <= 2)
+        uint32_t ni = 0, nCv = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            ni += interior[k];
+            nCv += interior[k] * (1u + (k >= 1) + (k <= 2));
         }
         auto ldv = [&](uint64_t r, bool &ok) {
             const uint64_t a = in + 4 * (r * pitch + c);
@@ -92,13 +99,12 @@ __global__ void __launch_bounds__(kThreads) k_stencil(const __grid_constant__ Fe
                         const float we = __fadd_rn(w, e);
                         const float s = __fadd_rn(ns, we);
                         o[k] = __fmaf_rn(c1, s, __fmul_rn(c0, cc[k]));
-                        if constexpr (MODE == kCheck) {
-                            if (interior[k]) {
-                                nv += (!okN) + (!okS[g]) + (!okCC);
-                                nv += (k == 0) ? (!okW[g]) : (!okCC);
-                                nv += (k == 3) ? (!okE[g]) : (!okCC);
-                            }
-                        }
+                    }
+                    if constexpr (MODE == kCheck) {
+                        // per interior point: N, S, C loads; W from the own vector
+                        // unless k == 0; E from the own vector unless k == 3
+                        nv += ni * ((uint32_t)!okN + (uint32_t)!okS[g]) + nCv * (uint32_t)!okCC +
+                              (uint32_t)!okW[g] + (uint32_t)!okE[g];
                     }
                     const uint64_t ao = out + 4 * (rr * pitch + c);
                     if (all4) {

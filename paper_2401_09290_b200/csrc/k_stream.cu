@@ -1,12 +1,16 @@
 // k_stream.cu -- fenced streaming kernels (SURVEY.md §2.7 K1 copy, K2 saxpy,
 // K7 partition fill) for sm_100a.
 //
-// HBM-bound: 128-bit LDG/STG, x4 unrolled with all loads issued before the
-// stores, persistent grid of (#SMs x resident CTAs).  Every 16-byte access
-// address goes through the fence of MODE (fence.cuh); the byte / element
-// tail uses the fence at its own width.  The fence costs 2 LOP3 (mask) or a
-// 64-bit subtract + LOP3 + compare (check) per 16 bytes -- far below the
-// integer throughput an SM has left while it waits on HBM.
+// HBM-bound.  Each CTA owns one contiguous chunk of kThreads x kU 16-byte
+// vectors (64 KB of copy traffic), issues all kU 128-bit loads per thread
+// before the stores, and the grid covers the whole tensor in one shot: the
+// design probe (tools/stream_variants.cu, profiles/) measured 6.9 TB/s for
+// this schedule against 5.9 TB/s for a persistent grid-stride loop.
+// Every 16-byte access address goes through the fence of MODE (fence.cuh);
+// the byte / element tail uses the fence at its own width.  The mask fence
+// is 2 LOP3 per 16 bytes; check mode hoists one range test per CTA chunk and
+// falls back to per-access checks only for chunks that touch the partition
+// edge (identical results: see range_in).
 #include "fence.cuh"
 #include "kernels.h"
 
@@ -14,7 +18,8 @@ namespace gd {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;
+constexpr int kU = 4;
+constexpr uint64_t kChunk = (uint64_t)kThreads * kU;   // vectors per CTA
 
 __device__ __forceinline__ uint4 ld16(uint64_t a) { return __ldcs(reinterpret_cast<const uint4 *>(a)); }
 __device__ __forceinline__ void st16(uint64_t a, uint4 v) { __stcs(reinterpret_cast<uint4 *>(a), v); }
@@ -26,40 +31,49 @@ __device__ __forceinline__ void st16f(uint64_t a, float4 v) { __stcs(reinterpret
 // unit one load + one store; per tail byte one load + one store.
 // ---------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ FenceDesc fd, uint64_t dst,
-                                                   uint64_t src, uint64_t nvec, uint32_t tail) {
+__device__ __forceinline__ void copy_chunk(const FenceDesc &fd, uint64_t dst, uint64_t src, uint64_t v0,
+                                           uint64_t nvec, uint32_t &nv) {
     const Fence<MODE, 16> f(fd);
-    uint32_t nv = 0;
-    const uint64_t T = (uint64_t)gridDim.x * kThreads;
-    uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    for (; v + (kUnroll - 1) * T < nvec; v += kUnroll * T) {
-        uint4 r[kUnroll];
+    uint4 r[kU];
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-            const uint64_t a = src + 16 * (v + u * T);
-            r[u] = make_uint4(0, 0, 0, 0);
+    for (int u = 0; u < kU; u++) {
+        const uint64_t v = v0 + u * kThreads;
+        r[u] = make_uint4(0, 0, 0, 0);
+        if (v < nvec) {
+            const uint64_t a = src + 16 * v;
             if (f.ok(a)) r[u] = ld16(f.addr(a));
             else nv++;
         }
+    }
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-            const uint64_t a = dst + 16 * (v + u * T);
+    for (int u = 0; u < kU; u++) {
+        const uint64_t v = v0 + u * kThreads;
+        if (v < nvec) {
+            const uint64_t a = dst + 16 * v;
             if (f.ok(a)) st16(f.addr(a), r[u]);
             else nv++;
         }
     }
-    for (; v < nvec; v += T) {
-        const uint64_t as = src + 16 * v, ad = dst + 16 * v;
-        uint4 r = make_uint4(0, 0, 0, 0);
-        if (f.ok(as)) r = ld16(f.addr(as));
-        else nv++;
-        if (f.ok(ad)) st16(f.addr(ad), r);
-        else nv++;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ FenceDesc fd, uint64_t dst,
+                                                   uint64_t src, uint64_t nvec, uint32_t tail) {
+    uint32_t nv = 0;
+    const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
+    const uint64_t v0 = c0 + threadIdx.x;
+    if constexpr (MODE == kCheck) {
+        const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
+        if (cn && range_in(fd, src + 16 * c0, 16 * cn) && range_in(fd, dst + 16 * c0, 16 * cn))
+            copy_chunk<kNone>(fd, dst, src, v0, nvec, nv);
+        else
+            copy_chunk<kCheck>(fd, dst, src, v0, nvec, nv);
+    } else {
+        copy_chunk<MODE>(fd, dst, src, v0, nvec, nv);
     }
-    const uint64_t tid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (tid < tail) {
+    if (blockIdx.x == 0 && threadIdx.x < tail) {
         const Fence<MODE, 1> f1(fd);
-        const uint64_t as = src + 16 * nvec + tid, ad = dst + 16 * nvec + tid;
+        const uint64_t as = src + 16 * nvec + threadIdx.x, ad = dst + 16 * nvec + threadIdx.x;
         uint8_t b = 0;
         if (f1.ok(as)) b = *reinterpret_cast<const uint8_t *>(f1.addr(as));
         else nv++;
@@ -76,49 +90,54 @@ __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ Fence
 // either wholly inside or wholly outside it).
 // ---------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_saxpy(const __grid_constant__ FenceDesc fd, float alpha,
-                                                    uint64_t x, uint64_t y, uint64_t nvec, uint32_t tail) {
+__device__ __forceinline__ void saxpy_chunk(const FenceDesc &fd, float alpha, uint64_t x, uint64_t y, uint64_t v0,
+                                            uint64_t nvec, uint32_t &nv) {
     const Fence<MODE, 16> f(fd);
-    uint32_t nv = 0;
-    const uint64_t T = (uint64_t)gridDim.x * kThreads;
-    uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    auto fma4 = [alpha](float4 a, float4 b) {
-        return make_float4(__fmaf_rn(alpha, a.x, b.x), __fmaf_rn(alpha, a.y, b.y), __fmaf_rn(alpha, a.z, b.z),
-                           __fmaf_rn(alpha, a.w, b.w));
-    };
-    for (; v + (kUnroll - 1) * T < nvec; v += kUnroll * T) {
-        float4 xv[kUnroll], yv[kUnroll];
+    float4 xv[kU], yv[kU];
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-            const uint64_t ax = x + 16 * (v + u * T), ay = y + 16 * (v + u * T);
-            xv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            yv[u] = xv[u];
+    for (int u = 0; u < kU; u++) {
+        const uint64_t v = v0 + u * kThreads;
+        xv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        yv[u] = xv[u];
+        if (v < nvec) {
+            const uint64_t ax = x + 16 * v, ay = y + 16 * v;
             if (f.ok(ax)) xv[u] = ld16f(f.addr(ax));
             else nv += 4;
             if (f.ok(ay)) yv[u] = ld16f(f.addr(ay));
             else nv += 4;
         }
+    }
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-            const uint64_t ay = y + 16 * (v + u * T);
-            if (f.ok(ay)) st16f(f.addr(ay), fma4(xv[u], yv[u]));
+    for (int u = 0; u < kU; u++) {
+        const uint64_t v = v0 + u * kThreads;
+        if (v < nvec) {
+            const uint64_t ay = y + 16 * v;
+            const float4 r = make_float4(__fmaf_rn(alpha, xv[u].x, yv[u].x), __fmaf_rn(alpha, xv[u].y, yv[u].y),
+                                         __fmaf_rn(alpha, xv[u].z, yv[u].z), __fmaf_rn(alpha, xv[u].w, yv[u].w));
+            if (f.ok(ay)) st16f(f.addr(ay), r);
             else nv += 4;
         }
     }
-    for (; v < nvec; v += T) {
-        const uint64_t ax = x + 16 * v, ay = y + 16 * v;
-        float4 xv = make_float4(0.f, 0.f, 0.f, 0.f), yv = xv;
-        if (f.ok(ax)) xv = ld16f(f.addr(ax));
-        else nv += 4;
-        if (f.ok(ay)) yv = ld16f(f.addr(ay));
-        else nv += 4;
-        if (f.ok(ay)) st16f(f.addr(ay), fma4(xv, yv));
-        else nv += 4;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_saxpy(const __grid_constant__ FenceDesc fd, float alpha,
+                                                    uint64_t x, uint64_t y, uint64_t nvec, uint32_t tail) {
+    uint32_t nv = 0;
+    const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
+    const uint64_t v0 = c0 + threadIdx.x;
+    if constexpr (MODE == kCheck) {
+        const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
+        if (cn && range_in(fd, x + 16 * c0, 16 * cn) && range_in(fd, y + 16 * c0, 16 * cn))
+            saxpy_chunk<kNone>(fd, alpha, x, y, v0, nvec, nv);
+        else
+            saxpy_chunk<kCheck>(fd, alpha, x, y, v0, nvec, nv);
+    } else {
+        saxpy_chunk<MODE>(fd, alpha, x, y, v0, nvec, nv);
     }
-    const uint64_t tid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (tid < tail) {
+    if (blockIdx.x == 0 && threadIdx.x < tail) {
         const Fence<MODE, 4> f4(fd);
-        const uint64_t ax = x + 16 * nvec + 4 * tid, ay = y + 16 * nvec + 4 * tid;
+        const uint64_t ax = x + 16 * nvec + 4 * threadIdx.x, ay = y + 16 * nvec + 4 * threadIdx.x;
         float xs = 0.f, ys = 0.f;
         if (f4.ok(ax)) xs = *reinterpret_cast<const float *>(f4.addr(ax));
         else nv++;
@@ -137,8 +156,11 @@ __global__ void __launch_bounds__(kThreads) k_saxpy(const __grid_constant__ Fenc
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_fill(uint64_t base, uint64_t offset, uint64_t nvec,
                                                    uint32_t pattern) {
-    const uint64_t T = (uint64_t)gridDim.x * kThreads;
-    for (uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x; v < nvec; v += T) {
+    const uint64_t v0 = (uint64_t)blockIdx.x * kChunk + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+        const uint64_t v = v0 + u * kThreads;
+        if (v >= nvec) break;
         const uint64_t o = offset + 16 * v;
         uint4 w = make_uint4(0, 0, 0, 0);
         if (pattern == 1) {
@@ -149,66 +171,48 @@ __global__ void __launch_bounds__(kThreads) k_fill(uint64_t base, uint64_t offse
     }
 }
 
-template <typename K>
-int blocks_per_sm(K kernel) {
-    int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1) b = 1;
-    return b;
-}
-
-uint64_t grid_for(uint64_t work_items, int sms, int bps) {
-    uint64_t want = (work_items + kThreads - 1) / kThreads;
-    uint64_t cap = (uint64_t)sms * (uint64_t)bps;
-    if (want > cap) want = cap;
-    return want ? want : 1;
+unsigned grid_for(uint64_t nvec) {
+    const uint64_t g = (nvec + kChunk - 1) / kChunk;
+    return (unsigned)(g ? g : 1);
 }
 
 template <int MODE>
-cudaError_t copy_t(const FenceDesc &fd, uint64_t dst, uint64_t src, uint64_t nbytes, cudaStream_t s,
-                   const Geom &g) {
-    static const int bps = blocks_per_sm(k_copy<MODE>);
+cudaError_t copy_t(const FenceDesc &fd, uint64_t dst, uint64_t src, uint64_t nbytes, cudaStream_t s) {
     const uint64_t nvec = nbytes / 16;
-    const uint32_t tail = (uint32_t)(nbytes % 16);
-    k_copy<MODE><<<(unsigned)grid_for(nvec / kUnroll + 1, g.sms, bps), kThreads, 0, s>>>(fd, dst, src, nvec, tail);
+    k_copy<MODE><<<grid_for(nvec), kThreads, 0, s>>>(fd, dst, src, nvec, (uint32_t)(nbytes % 16));
     return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t saxpy_t(const FenceDesc &fd, float alpha, uint64_t x, uint64_t y, uint64_t n, cudaStream_t s,
-                    const Geom &g) {
-    static const int bps = blocks_per_sm(k_saxpy<MODE>);
+cudaError_t saxpy_t(const FenceDesc &fd, float alpha, uint64_t x, uint64_t y, uint64_t n, cudaStream_t s) {
     const uint64_t nvec = n / 4;
-    const uint32_t tail = (uint32_t)(n % 4);
-    k_saxpy<MODE><<<(unsigned)grid_for(nvec / kUnroll + 1, g.sms, bps), kThreads, 0, s>>>(fd, alpha, x, y, nvec,
-                                                                                         tail);
+    k_saxpy<MODE><<<grid_for(nvec), kThreads, 0, s>>>(fd, alpha, x, y, nvec, (uint32_t)(n % 4));
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_copy(int mode, const FenceDesc &fd, uint64_t dst, uint64_t src, uint64_t nbytes,
-                        cudaStream_t s, const Geom &g) {
+                        cudaStream_t s, const Geom &) {
     switch (mode) {
-        case kNone: return copy_t<kNone>(fd, dst, src, nbytes, s, g);
-        case kMask: return copy_t<kMask>(fd, dst, src, nbytes, s, g);
-        default: return copy_t<kCheck>(fd, dst, src, nbytes, s, g);
+        case kNone: return copy_t<kNone>(fd, dst, src, nbytes, s);
+        case kMask: return copy_t<kMask>(fd, dst, src, nbytes, s);
+        default: return copy_t<kCheck>(fd, dst, src, nbytes, s);
     }
 }
 
 cudaError_t launch_saxpy(int mode, const FenceDesc &fd, float alpha, uint64_t x, uint64_t y, uint64_t n,
-                         cudaStream_t s, const Geom &g) {
+                         cudaStream_t s, const Geom &) {
     switch (mode) {
-        case kNone: return saxpy_t<kNone>(fd, alpha, x, y, n, s, g);
-        case kMask: return saxpy_t<kMask>(fd, alpha, x, y, n, s, g);
-        default: return saxpy_t<kCheck>(fd, alpha, x, y, n, s, g);
+        case kNone: return saxpy_t<kNone>(fd, alpha, x, y, n, s);
+        case kMask: return saxpy_t<kMask>(fd, alpha, x, y, n, s);
+        default: return saxpy_t<kCheck>(fd, alpha, x, y, n, s);
     }
 }
 
 cudaError_t launch_fill(uint64_t base, uint64_t offset, uint64_t nbytes, uint32_t pattern, cudaStream_t s,
-                        const Geom &g) {
-    static const int bps = blocks_per_sm(k_fill);
-    const uint64_t nvec = nbytes / 16;
-    k_fill<<<(unsigned)grid_for(nvec, g.sms, bps), kThreads, 0, s>>>(base, offset, nvec, pattern);
+                        const Geom &) {
+    k_fill<<<grid_for(nbytes / 16), kThreads, 0, s>>>(base, offset, nbytes / 16, pattern);
     return cudaGetLastError();
 }
 

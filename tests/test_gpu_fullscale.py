@@ -1,0 +1,210 @@
+"""GPU parity at the BASELINE.json sizes, in the launch configuration bench.py
+and tools/kernel_bench.py time: 16 GiB partitions, C2 (4 GiB copy, 2^30
+saxpy), C3 (2^26 indices into a 2^29-entry table, 1 % OOB), C4 (32768^2
+stencil, 8192^3 GEMM).
+
+The oracle cannot simulate 16 GiB partitions whole, so each test checks
+(a) the exact check-mode violation count (the generator's planted count),
+(b) outputs the oracle computes one by one on sampled positions, and
+(c) properties that hold at any size (victims unchanged, in-bounds results
+equal a library routine, wrapped reads equal the address-revealing pattern's
+closed form).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2401_09290_b200 import devmem
+from tests.gpu_util import download
+
+pytestmark = pytest.mark.gpu
+
+GiB = 1 << 30
+PART = 1 << 34
+N_IDX, T_N = 1 << 26, 1 << 29
+IDX_OFF, OUT_OFF, PAT_OFF = 2 * GiB, 2 * GiB + GiB // 4, 2 * GiB + GiB // 2
+
+
+@pytest.fixture
+def two_tenants(arenas):
+    a = arenas(2 * PART)
+    victim = a.partition_alloc(PART)
+    p = a.partition_alloc(PART)
+    assert p.base == victim.base + PART              # raw j < 0 addresses land in the victim
+    return a, victim, p
+
+
+def _c3_inputs(a, p, seed, frac):
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(seed)
+    devmem.view(p.base, T_N, torch.int32).random_(generator=gen)                 # table
+    devmem.view(p.base + OUT_OFF, N_IDX, torch.int32).random_(generator=gen)     # out / src
+    a.fill(p.id, 1, PAT_OFF, PART - PAT_OFF)                                     # P(o) pattern
+    idx, pos = synth.indices_with_oob(synth.rng_for(seed), N_IDX, T_N, frac)
+    devmem.view(p.base + IDX_OFF, N_IDX, torch.int32).copy_(torch.from_numpy(idx))
+    torch.cuda.synchronize()
+    return idx, pos
+
+
+@pytest.mark.parametrize("mode", ["mask", "check"])
+def test_c3_gather_full(two_tenants, mode):
+    a, victim, p = two_tenants
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(3)
+    vview = devmem.view(victim.base, PART // 4, torch.int32)
+    vview.random_(generator=gen)
+    vcopy = vview.clone()
+    idx, pos = _c3_inputs(a, p, 3001, 0.01)
+    assert len(pos) == 671089
+    a.stats_reset()
+    a.gather(p.id, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, N_IDX)
+    st = a.stats(p.id)
+    out = devmem.view(p.base + OUT_OFF, N_IDX, torch.int32)
+    table = devmem.view(p.base, T_N, torch.int32)
+    idx_t = devmem.view(p.base + IDX_OFF, N_IDX, torch.int32).long()
+    inb = torch.ones(N_IDX, dtype=torch.bool, device="cuda")
+    pos_t = torch.from_numpy(pos).cuda()
+    inb[pos_t] = False
+    # (c) in-bounds results equal index_select; victims untouched
+    assert torch.equal(out[inb], table[idx_t[inb]])
+    assert torch.equal(vview, vcopy)
+    # (a) + (c) planted positions
+    if mode == "check":
+        assert st["violations"] == 671089
+        assert (out[pos_t] == 0).all()
+    else:
+        assert st["violations"] == 0
+        j = idx[pos].astype(np.int64)
+        expect = synth.pattern_words(np.mod(PART + 4 * j, PART).astype(np.uint64)).view(np.int32)
+        np.testing.assert_array_equal(out[pos_t].cpu().numpy(), expect)
+    # (b) oracle, one by one, on sampled positions (planted and in-bounds)
+    rng = synth.rng_for(7)
+    sample = np.concatenate([rng.choice(pos, 2000, replace=False), rng.integers(0, N_IDX, 2000)])
+    outs = out.cpu().numpy()
+    for i in sample:
+        ai, ok = oracle.resolve(p.base, p.size, mode, p.base + IDX_OFF + 4 * int(i), 4)
+        assert ok and ai == p.base + IDX_OFF + 4 * int(i)
+        r, ok = oracle.resolve(p.base, p.size, mode, (p.base + 4 * int(idx[i])) % 2**64, 4)
+        want = 0 if not ok else int(download(r, 4).view(np.int32)[0])
+        assert outs[i] == want, (i, idx[i], outs[i], want)
+
+
+@pytest.mark.parametrize("mode", ["mask", "check"])
+def test_c3_scatter_full(two_tenants, mode):
+    a, victim, p = two_tenants
+    idx, pos = _c3_inputs(a, p, 3002, 0.01)
+    before = devmem.view(p.base, PART // 4, torch.int32).clone()
+    a.stats_reset()
+    a.scatter(p.id, mode, p.base, p.base + IDX_OFF, p.base + OUT_OFF, N_IDX)
+    st = a.stats(p.id)
+    assert st["violations"] == (671089 if mode == "check" else 0)
+    after = devmem.view(p.base, PART // 4, torch.int32)
+    src = devmem.view(p.base + OUT_OFF, N_IDX, torch.int32).long() & 0xFFFFFFFF
+    idx_t = torch.from_numpy(idx.astype(np.int64)).cuda()
+    inb = torch.ones(N_IDX, dtype=torch.bool, device="cuda")
+    pos_t = torch.from_numpy(pos).cuda()
+    inb[pos_t] = False
+    # table region: index_add_ reference (int64, reduced mod 2^32)
+    ref = before[:T_N].long() & 0xFFFFFFFF
+    ref.index_add_(0, idx_t[inb], src[inb])
+    assert torch.equal(after[:T_N].long() & 0xFFFFFFFF, ref & 0xFFFFFFFF)
+    del ref
+    if mode == "mask":
+        # planted indices: the oracle fences each raw address; the adds land there
+        raw = (p.base + 4 * idx[pos].astype(np.int64)).astype(np.uint64)
+        f = oracle.fence_mask_n(raw, p.base, p.size, 4)
+        words = torch.from_numpy(((f - np.uint64(p.base)) // np.uint64(4)).astype(np.int64)).cuda()
+        assert (words >= T_N).all()
+        u, inv = torch.unique(words, return_inverse=True)
+        sums = torch.zeros(u.numel(), dtype=torch.int64, device="cuda").index_add_(0, inv, src[pos_t])
+        want = (before[u].long() + sums) & 0xFFFFFFFF
+        assert torch.equal(after[u].long() & 0xFFFFFFFF, want)
+        after[u] = before[u]                         # then nothing else may differ
+    assert torch.equal(after[T_N:], before[T_N:])
+
+
+def test_c2_copy_saxpy_full(arenas):
+    a = arenas(PART)
+    p = a.partition_alloc(PART)
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(2000)
+    src = devmem.view(p.base, GiB, torch.int32)
+    src.random_(generator=gen)
+    x = devmem.view(p.base + 8 * GiB, 1 << 30, torch.float32)
+    y = devmem.view(p.base + 12 * GiB, 1 << 30, torch.float32)
+    x.uniform_(-1, 1, generator=gen)
+    y.uniform_(-1, 1, generator=gen)
+    y0 = y.clone()
+    a.stats_reset()
+    a.copy(p.id, "mask", p.base + 4 * GiB, p.base, 4 * GiB)
+    a.saxpy(p.id, "check", 1.5, p.base + 8 * GiB, p.base + 12 * GiB, 1 << 30)
+    assert a.stats(p.id)["violations"] == 0
+    assert torch.equal(devmem.view(p.base + 4 * GiB, GiB, torch.int32), src)
+    # saxpy: 1M sampled elements through the oracle
+    rng = synth.rng_for(8)
+    s = torch.from_numpy(rng.integers(0, 1 << 30, 1 << 20)).cuda()
+    xs, ys, got = x[s].cpu().numpy(), y0[s].cpu().numpy(), y[s].cpu().numpy()
+    m = oracle.Mem(0x10000000, 8 << 20)
+    m.write(0x10000000, xs)
+    m.write(0x10000000 + (4 << 20), ys)
+    oracle.saxpy(m, 0x10000000, 8 << 20, "none", 1.5, 0x10000000, 0x10000000 + (4 << 20), 1 << 20)
+    np.testing.assert_array_equal(got.view(np.uint32), m.view(0x10000000 + (4 << 20), np.uint32, 1 << 20))
+
+
+def test_c4_stencil_full_sampled_rows(arenas):
+    a = arenas(PART)
+    p = a.partition_alloc(PART)
+    H = W = 32768
+    inp, out = p.base + 4 * GiB, p.base + 8 * GiB
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(4000)
+    devmem.view(inp, H * W, torch.float32).uniform_(0, 1, generator=gen)
+    a.stencil(p.id, "mask", out, inp, H, W, W, 0.5, 0.125)
+    rng = synth.rng_for(9)
+    rows = np.concatenate([[1, 2, 63, 64, 65, H - 2], rng.integers(1, H - 1, 20)])
+    for r in rows:
+        band = download(inp + 4 * (int(r) - 1) * W, 3 * 4 * W)
+        m = oracle.Mem(0x20000000, 4 << 20)
+        m.buf[:band.size] = band
+        oracle.stencil(m, 0x20000000, 4 << 20, "none", 0x20000000 + (2 << 20), 0x20000000, 3, W, W, 0.5, 0.125)
+        want = m.view(0x20000000 + (2 << 20) + 4 * W, np.uint32, W)[1:W - 1]
+        got = download(out + 4 * int(r) * W, 4 * W).view(np.uint32)[1:W - 1]
+        np.testing.assert_array_equal(got, want, err_msg=f"row {r}")
+
+
+@pytest.mark.parametrize("clamp", [False, True])
+def test_c4_gemm_8192_sampled_rows(arenas, clamp):
+    a = arenas(PART)
+    p = a.partition_alloc(PART)
+    n, MiB = 8192, 1 << 20
+    if clamp:                                   # A's last 64 rows lie past end
+        A = p.end - (n - 64) * n * 2
+        B, C = A - 160 * MiB, A - 320 * MiB
+    else:
+        A, B, C = p.base, p.base + 160 * MiB, p.base + 320 * MiB
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(4001)
+    devmem.view(A, (n - 64) * n if clamp else n * n, torch.bfloat16).uniform_(-1, 1, generator=gen)
+    devmem.view(B, n * n, torch.bfloat16).uniform_(-1, 1, generator=gen)
+    mode = "check" if clamp else "mask"
+    a.stats_reset()
+    a.gemm(p.id, mode, C, A, B, n, n, n, n, n, n)
+    assert a.device_flags() == 0
+    assert a.stats(p.id)["violations"] == (64 if clamp else 0)
+    rng = synth.rng_for(10)
+    rows = np.unique(np.concatenate([[0, 127, 128, n - 65, n - 64, n - 1], rng.integers(0, n, 6)])).astype(np.uint32)
+    lo = min(A, B, C)
+    hi = p.end if clamp else max(A, B, C) + 2 * n * n
+    mem = oracle.Mem(lo, buf=download(lo, hi - lo))
+    gpu_c = download(C, 2 * n * n).view(np.uint16).reshape(n, n)
+    c = oracle.gemm(mem, p.base, p.size, mode, C, A, B, n, n, n, n, n, n, rows=rows)
+    assert c.faults == 0
+    ref_c = mem.view(C, np.uint16, n * n).reshape(n, n)
+    g = (gpu_c[rows].astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    r = (ref_c[rows].astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    rel = np.linalg.norm(g - r) / max(np.linalg.norm(r), 1e-30)
+    assert rel <= 1e-2, rel
+    if clamp:
+        assert (gpu_c[n - 64:] == 0).all()

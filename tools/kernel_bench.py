@@ -39,19 +39,29 @@ def paper_mean(xs):
     return statistics.mean(core)
 
 
-def time_modes(launch, reps, warm=3):
-    """launch(mode, stream) -> None; interleaved none/mask/check."""
+def time_modes(launch, reps, warm=3, extra=None):
+    """launch(mode, stream) -> None; interleaved none/mask/check (+ extra
+    reference launches {name: fn(stream)} timed in the same rotation)."""
     s = torch.cuda.Stream()
     res = {m: [] for m in ("none", "mask", "check")}
+    extra = extra or {}
+    res.update({k: [] for k in extra})
+
+    def go(m):
+        if m in extra:
+            extra[m](s)
+        else:
+            launch(m, s)
+
     with torch.cuda.stream(s):
         for m in res:
             for _ in range(warm):
-                launch(m, s)
+                go(m)
         for _ in range(reps):
             for m in res:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(s)
-                launch(m, s)
+                go(m)
                 b.record(s)
                 b.synchronize()
                 res[m].append(a.elapsed_time(b))
@@ -149,21 +159,16 @@ def main():
         A, B, C = b, b + n * n * 2, b + 2 * n * n * 2
         devmem.view(A, n * n, torch.bfloat16).uniform_(-1, 1, generator=gen)
         devmem.view(B, n * n, torch.bfloat16).uniform_(-1, 1, generator=gen)
-        r = time_modes(lambda m, s: arena.gemm(p.id, m, C, A, B, n, n, n, n, n, n, stream=s), max(4, args.reps // 2))
-        res = summarize("gemm 8192^3 bf16", r, 2 * n ** 3, "TFLOP/s", bf16)
         ta = devmem.view(A, n * n, torch.bfloat16).view(n, n)
         tb = devmem.view(B, n * n, torch.bfloat16).view(n, n)
-        xs = []
-        for i in range(3 + max(4, args.reps // 2)):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            torch.matmul(ta, tb.t())
-            e1.record()
-            e1.synchronize()
-            if i >= 3:
-                xs.append(e0.elapsed_time(e1))
+        tc = torch.empty(n, n, dtype=torch.bfloat16, device="cuda")
+        r = time_modes(lambda m, s: arena.gemm(p.id, m, C, A, B, n, n, n, n, n, n, stream=s), args.reps,
+                       extra={"torch": lambda s: torch.matmul(ta, tb.t(), out=tc)})
+        xs = r.pop("torch")
+        res = summarize("gemm 8192^3 bf16", r, 2 * n ** 3, "TFLOP/s", bf16)
         res["torch_matmul"] = {"ms_median": round(statistics.median(xs), 4),
-                               "TFLOP/s": round(2 * n ** 3 / (statistics.median(xs) / 1e3) / 1e12, 1)}
+                               "TFLOP/s": round(2 * n ** 3 / (statistics.median(xs) / 1e3) / 1e12, 1),
+                               "note": "cuBLAS via torch.matmul, timed interleaved with the fenced GEMM"}
         print(f"  torch.matmul: {res['torch_matmul']['TFLOP/s']} TFLOP/s", file=sys.stderr)
         results["gemm_8192^3"] = res
     results["device_flags"] = arena.device_flags()
