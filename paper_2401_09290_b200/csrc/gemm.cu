@@ -258,6 +258,208 @@ k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     }
 }
 
+// ---------------------------------------------------------------------------
+// 2-SM variant: a CTA pair (cluster of 2) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and
+// its 128 rows (N half) of B, so per-SM shared-memory traffic per MMA halves
+// for B -- the 1-SM kernel is shared-memory-bandwidth bound (TMA writes plus
+// tensor-core operand reads of 48 KB per 512 cycles).  The leader CTA (rank
+// 0) issues the MMAs; both CTAs' TMA loads complete on the leader's full
+// barrier, the leader's commits multicast to both CTAs' empty / tmem-full
+// barriers, and both CTAs' epilogue warps release the accumulator on the
+// leader's tmem-empty barrier.  Each CTA's TMEM holds its 128 rows x 256
+// fp32 columns per accumulator (2 accumulators, 512 columns).
+// ---------------------------------------------------------------------------
+constexpr uint32_t IDESC2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(2 * BM >> 4) << 24);
+constexpr uint32_t B_HALF = BN / 2;                           // B rows staged per CTA
+constexpr uint32_t STAGE2_BYTES = A_BYTES + B_HALF * BK * 2;  // 32 KB
+constexpr int STAGES2 = 6;
+constexpr uint32_t SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_to_cta(uint32_t saddr, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, uint64_t C, uint64_t ldc,
+        uint32_t N, uint32_t K, uint64_t rowsC, uint32_t tm, uint32_t tn) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *bars = (uint64_t *)(smem + STAGES2 * STAGE2_BYTES);
+    uint64_t *full = bars, *empty = bars + STAGES2;
+    uint64_t *tfull = bars + 2 * STAGES2, *tempty = bars + 2 * STAGES2 + ACC;
+    uint32_t *tmem_slot = (uint32_t *)(bars + 2 * STAGES2 + 2 * ACC);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const uint32_t nkb = K / BK, ntiles = tm * tn;      // tm counts 256-row pair tiles
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+        for (int s = 0; s < STAGES2; s++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(&full[s])));    // both producers
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
+        }
+        for (int a = 0; a < ACC; a++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tfull[a])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(smem_u32(&tempty[a])));  // 2 x 4 epilogue warps
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer (both CTAs) ----------------
+        uint32_t it = 0;
+        bool alive = true;
+        for (uint32_t t = pair; t < ntiles && alive; t += npairs) {
+            uint32_t mb, nb;
+            tile_coords(t, tm, tn, mb, nb);
+            const int row_a = (int)(mb * 2 * BM + rank * BM), row_b = (int)(nb * BN + rank * B_HALF);
+            for (uint32_t kb = 0; kb < nkb; kb++, it++) {
+                const uint32_t s = it % STAGES2, ph = (it / STAGES2) & 1;
+                if (!mbar_wait(smem_u32(&empty[s]), ph ^ 1)) { alive = false; break; }
+                const uint32_t fb = map_to_cta(smem_u32(&full[s]), 0);     // the leader's full barrier
+                // default (.release.cta) semantics: the transaction count is all the
+                // leader needs; a cluster-scope release would put a MEMBAR.GPU on
+                // every stage (measured: halves tensor-pipe activity)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(fb),
+                             "r"(STAGE2_BYTES)
+                             : "memory");
+                const uint32_t sa = smem_u32(smem + s * STAGE2_BYTES), sb = sa + A_BYTES;
+                const int kc = (int)(kb * BK);
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%3, %4}], [%2];" ::"r"(sa), "l"(&tmA), "r"(fb), "r"(kc), "r"(row_a)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%3, %4}], [%2];" ::"r"(sb), "l"(&tmB), "r"(fb), "r"(kc), "r"(row_b)
+                    : "memory");
+            }
+        }
+    } else if (warp == 1 && lane == 0 && rank == 0) {
+        // ---------------- MMA issuer (leader CTA only) ----------------
+        uint32_t it = 0, tl = 0;
+        bool alive = true;
+        for (uint32_t t = pair; t < ntiles && alive; t += npairs, tl++) {
+            const uint32_t acc = tl & 1, aph = (tl >> 1) & 1;
+            if (!mbar_wait(smem_u32(&tempty[acc]), aph ^ 1)) break;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t dacc = tmem + acc * BN;
+            for (uint32_t kb = 0; kb < nkb; kb++, it++) {
+                const uint32_t s = it % STAGES2, ph = (it / STAGES2) & 1;
+                if (!mbar_wait(smem_u32(&full[s]), ph)) { alive = false; break; }
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t sa = smem_u32(smem + s * STAGE2_BYTES), sb = sa + A_BYTES;
+#pragma unroll
+                for (int k = 0; k < BK / 16; k++) {
+                    const uint64_t da = sw128_desc(sa + 32 * k), db = sw128_desc(sb + 32 * k);
+                    const uint32_t accum = (kb | k) ? 1u : 0u;
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                        ::"r"(dacc), "l"(da), "l"(db), "r"(IDESC2), "r"(accum)
+                        : "memory");
+                }
+                asm volatile(
+                    "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                    ::"r"(smem_u32(&empty[s])), "h"((uint16_t)3)
+                    : "memory");
+            }
+            asm volatile(
+                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                ::"r"(smem_u32(&tfull[acc])), "h"((uint16_t)3)
+                : "memory");
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue (both CTAs: own 128 rows) ----------------
+        const uint32_t wq = warp - 4;
+        uint32_t tl = 0;
+        for (uint32_t t = pair; t < ntiles; t += npairs, tl++) {
+            uint32_t mb, nb;
+            tile_coords(t, tm, tn, mb, nb);
+            const uint32_t acc = tl & 1, aph = (tl >> 1) & 1;
+            if (!mbar_wait(smem_u32(&tfull[acc]), aph)) break;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t row = (uint64_t)mb * 2 * BM + rank * BM + wq * 32 + lane;
+            const bool store_row = row < rowsC;
+            const uint32_t n0 = nb * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; c++) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((wq * 32u) << 16) + acc * BN + (uint32_t)(c * 32);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c == BN / 32 - 1) {
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        const uint32_t tb = map_to_cta(smem_u32(&tempty[acc]), 0);   // the leader's barrier
+                        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tb)
+                                     : "memory");
+                    }
+                }
+                if (store_row) {
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const uint32_t col = n0 + c * 32 + q * 8;
+                        if (col < N) {
+                            uint32_t p[4];
+#pragma unroll
+                            for (int e = 0; e < 4; e++) {
+                                __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * e]),
+                                                                         __uint_as_float(v[q * 8 + 2 * e + 1]));
+                                p[e] = *reinterpret_cast<uint32_t *>(&h);
+                            }
+                            uint4 *dst = reinterpret_cast<uint4 *>(C + 2 * (row * ldc + col));
+                            *dst = make_uint4(p[0], p[1], p[2], p[3]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();                 // no CTA leaves while its peer may still signal it
+    if (warp == 2) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
 __global__ void k_add_violations(unsigned long long *viol, unsigned long long n) { atomicAdd(viol, n); }
 
 // 2-D bf16 tensor map: inner dim = K (contiguous), outer = rows.
@@ -334,9 +536,25 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
     std::memset(&tmB, 0, sizeof(tmB));
     if (!make_map(&tmA, Af, K, rA, ldA, BM) || !make_map(&tmB, Bf, K, rB, ldB, BN)) return GD_ERR_UNSUPPORTED;
     static bool attr = [] {
-        return cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) == cudaSuccess;
+        return cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) == cudaSuccess &&
+               cudaFuncSetAttribute(k_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES) == cudaSuccess;
     }();
     if (!attr) return cuda_status(cudaErrorInvalidValue);
+    static const int force1 = [] {
+        const char *e = getenv("GD_GEMM_1SM");
+        return e && e[0] == '1';
+    }();
+    if (rC >= 2 * BM && !force1 && g.sms >= 2) {
+        // 2-SM path: B staged in N halves per CTA
+        CUtensorMap tmB2;
+        std::memset(&tmB2, 0, sizeof(tmB2));
+        if (!make_map(&tmB2, Bf, K, rB, ldB, B_HALF)) return GD_ERR_UNSUPPORTED;
+        const uint32_t tm = (uint32_t)((rC + 2 * BM - 1) / (2 * BM)), tn = (N + BN - 1) / BN;
+        const uint32_t ntiles = tm * tn, pairs_max = (uint32_t)g.sms / 2;
+        const uint32_t grid = 2 * (ntiles < pairs_max ? ntiles : pairs_max);
+        k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, Cf, ldc, N, K, rC, tm, tn);
+        return cuda_status(cudaGetLastError());
+    }
     const uint32_t tm = (uint32_t)((rC + BM - 1) / BM), tn = (N + BN - 1) / BN;   // rC <= M
     const uint32_t ntiles = tm * tn;
     const uint32_t grid = ntiles < (uint32_t)g.sms ? ntiles : (uint32_t)g.sms;

@@ -80,6 +80,43 @@ extern "C" int svariant_run(uint64_t base, uint64_t mask, uint64_t table, uint64
     return (int)cudaGetLastError();
 }
 
+// random reads of WB bytes (WB/16 16-byte vectors, or one 4/8-byte word) at
+// WB-aligned random positions of a 2 GiB table: accesses/s vs access size
+template <int WB>
+__global__ void __launch_bounds__(256) r_read(uint64_t table, uint64_t idx, uint64_t n, uint64_t slots,
+                                              uint32_t *sink) {
+    const uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t j = __ldcs(reinterpret_cast<const uint32_t *>(idx) + i) % (uint32_t)slots;
+    const uint64_t a = table + (uint64_t)j * WB;
+    uint32_t acc = 0;
+    if constexpr (WB == 4) acc = __ldcg(reinterpret_cast<const uint32_t *>(a));
+    else if constexpr (WB == 8) { uint2 v = __ldcg(reinterpret_cast<const uint2 *>(a)); acc = v.x ^ v.y; }
+    else {
+#pragma unroll
+        for (int q = 0; q < WB / 16; q++) {
+            uint4 v = __ldcg(reinterpret_cast<const uint4 *>(a) + q);
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    }
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
+extern "C" int rread_run(int wb, uint64_t table, uint64_t idx, uint64_t n, void *sink, void *stream) {
+    const uint64_t slots = (2ull << 30) / wb;
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned g = (unsigned)((n + 255) / 256);
+    switch (wb) {
+        case 4: r_read<4><<<g, 256, 0, s>>>(table, idx, n, slots, (uint32_t *)sink); break;
+        case 8: r_read<8><<<g, 256, 0, s>>>(table, idx, n, slots, (uint32_t *)sink); break;
+        case 16: r_read<16><<<g, 256, 0, s>>>(table, idx, n, slots, (uint32_t *)sink); break;
+        case 32: r_read<32><<<g, 256, 0, s>>>(table, idx, n, slots, (uint32_t *)sink); break;
+        case 64: r_read<64><<<g, 256, 0, s>>>(table, idx, n, slots, (uint32_t *)sink); break;
+        case 128: r_read<128><<<g, 256, 0, s>>>(table, idx, n, slots, (uint32_t *)sink); break;
+    }
+    return (int)cudaGetLastError();
+}
+
 extern "C" int gvariant_count() { return 9; }
 extern "C" const char *gvariant_name(int v) {
     static const char *n[] = {"ldg U2", "ldcg U2", "ldcs U2", "nc.no_alloc U2", "no_alloc U2", "relaxed.gpu U2",

@@ -54,6 +54,26 @@ def main():
             res[key] = {"ms": round(ms, 4), "Gidx_per_s": round(n / (ms / 1e3) / 1e9, 2)}
             print(f"{key:34s} {ms:8.4f} ms {res[key]['Gidx_per_s']} Gidx/s", file=sys.stderr)
     L.set_l2_fetch(128)
+    L.rread_run.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
+                            ctypes.c_void_p]
+    sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+    iv.random_()
+    for wb in (4, 8, 16, 32, 64, 128):
+        ts = []
+        for i in range(13):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            assert L.rread_run(wb, table, idx, n, sink.data_ptr(), s.cuda_stream) == 0
+            b.record()
+            b.synchronize()
+            if i >= 3:
+                ts.append(a.elapsed_time(b))
+        ms = statistics.median(ts)
+        key = f"random read {wb} B"
+        res[key] = {"ms": round(ms, 4), "Gaccess_per_s": round(n / (ms / 1e3) / 1e9, 2),
+                    "useful_GBps": round(n * wb / (ms / 1e3) / 1e9, 1)}
+        print(f"{key:24s} {ms:8.4f} ms {res[key]['Gaccess_per_s']} Gacc/s {res[key]['useful_GBps']} GB/s useful",
+              file=sys.stderr)
     for v in range(L.gvariant_count()):
         ts = []
         for i in range(13):
