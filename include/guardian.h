@@ -60,8 +60,16 @@ typedef enum {
  *  CHECK : address checking: an access is allowed iff its
  *          w bytes lie in [base, base+size) and it is w-aligned; a refused
  *          load reads 0, a refused store / atomic is dropped, and the
- *          tenant's violation counter is incremented (reading A1).          */
-typedef enum { GD_MODE_NONE = 0, GD_MODE_MASK = 1, GD_MODE_CHECK = 2 } gd_mode;
+ *          tenant's violation counter is incremented (reading A1).
+ *  MODULO: address fencing with modulo (§4.4), fenced =
+ *          base + (((addr - base) mod size) & ~(w-1)), the 64-bit modulo
+ *          inline with the reciprocal parameter floor(2^64/size) ("an extra
+ *          parameter holding the 1/partition_size").  Needs no
+ *          alignment and no power-of-two size: it is the mode for exact-size
+ *          partitions (gd_partition_alloc_exact).  Nothing is detected.
+ *  MASK requires a power-of-two, size-aligned partition (GD_ERR_NOT_POW2
+ *  otherwise); NONE, CHECK and MODULO take any partition.      */
+typedef enum { GD_MODE_NONE = 0, GD_MODE_MASK = 1, GD_MODE_CHECK = 2, GD_MODE_MODULO = 3 } gd_mode;
 
 /* Kernel kinds (index of the per-kind statistics).                            */
 typedef enum {
@@ -81,10 +89,12 @@ typedef struct gd_arena gd_arena;     /* opaque, library-owned */
 
 /* One row of the partition bounds table ("the application id,
  * the base address, and the partition size"); mask and end are derived
- * (PAPER.md:230).  base is aligned to size; size is a power of two.          */
+ * (PAPER.md:230).  For GD_PART_POW2 partitions base is aligned to size and
+ * size is a power of two; exact-size partitions carry only base and size.   */
+#define GD_PART_POW2 1u
 typedef struct {
     uint32_t id;
-    uint32_t reserved;
+    uint32_t flags;                   /* GD_PART_POW2 or 0          */
     uint64_t base;
     uint64_t size;
     uint64_t mask;                    /* size - 1                  */
@@ -127,6 +137,14 @@ gd_status gd_arena_info(const gd_arena *a, uint64_t *base, uint64_t *size, int *
  * Errors: INVALID_ARG (requested 0 or > arena), DEVICE_OOM (no free block,
  * or all GD_MAX_TENANTS ids in use), CUDA.                                    */
 gd_status gd_partition_alloc(gd_arena *a, uint64_t requested_bytes, gd_partition_info *out);
+/* Exact-size partition (removes the power-of-two
+ * utilisation limit PAPER.md:246 names): size = requested rounded up to the
+ * physical backing granule (2 MiB for VMM arenas, 4 KiB otherwise); placed at
+ * a block of next_pow2(size) whose unused tail goes straight back to the
+ * buddy allocator.  Usable with NONE, CHECK and MODULO launches; a MASK
+ * launch on it returns GD_ERR_NOT_POW2 (unless size happens to be a power
+ * of two).  Errors as gd_partition_alloc.                                   */
+gd_status gd_partition_alloc_exact(gd_arena *a, uint64_t requested_bytes, gd_partition_info *out);
 /* Return a partition to the buddy allocator (coalescing). UNKNOWN_PARTITION. */
 gd_status gd_partition_free(gd_arena *a, uint32_t id);
 gd_status gd_partition_get(const gd_arena *a, uint32_t id, gd_partition_info *out);

@@ -22,8 +22,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
-NONE, MASK, CHECK = 0, 1, 2
-MODES = {"none": NONE, "mask": MASK, "check": CHECK}
+NONE, MASK, CHECK, MODULO = 0, 1, 2, 3
+MODES = {"none": NONE, "mask": MASK, "check": CHECK, "modulo": MODULO}
 
 
 class OrCtx(ctypes.Structure):
@@ -70,6 +70,10 @@ def lib():
         L.or_mask.argtypes = [u64]
         L.or_fence_mask.restype = u64
         L.or_fence_mask.argtypes = [u64, u64, u64, u32]
+        L.or_fence_modulo.restype = u64
+        L.or_fence_modulo.argtypes = [u64, u64, u64, u32]
+        L.or_fence_modulo_n.argtypes = [ctypes.c_void_p, u64, u64, u64, u32, ctypes.c_void_p]
+        L.or_fence_modulo_n.restype = None
         L.or_check_ok.restype = i32
         L.or_check_ok.argtypes = [u64, u64, u64, u32]
         L.or_check_range.restype = i32
@@ -103,6 +107,10 @@ def mask(size: int) -> int:
     return lib().or_mask(size)
 
 
+def fence_modulo(a: int, base: int, size: int, w: int = 1) -> int:
+    return lib().or_fence_modulo(a & (2**64 - 1), base, size, w)
+
+
 def fence_mask(a: int, base: int, size: int, w: int = 1) -> int:
     return lib().or_fence_mask(a & (2**64 - 1), base, size, w)
 
@@ -119,6 +127,13 @@ def fence_mask_n(a: np.ndarray, base: int, size: int, w: int = 1) -> np.ndarray:
     a = np.ascontiguousarray(a, dtype=np.uint64)
     out = np.empty_like(a)
     lib().or_fence_mask_n(a.ctypes.data, a.size, base, size, w, out.ctypes.data)
+    return out
+
+
+def fence_modulo_n(a: np.ndarray, base: int, size: int, w: int = 1) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    out = np.empty_like(a)
+    lib().or_fence_modulo_n(a.ctypes.data, a.size, base, size, w, out.ctypes.data)
     return out
 
 

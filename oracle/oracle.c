@@ -39,6 +39,15 @@ uint64_t or_fence_mask(uint64_t a, uint64_t base, uint64_t size, uint32_t w) {
     return r;
 }
 
+uint64_t or_fence_modulo(uint64_t a, uint64_t base, uint64_t size, uint32_t w) {
+    /* fenced_addr = partition_base +
+     * ((arbitrary_addr - partition_base) % partition_size)                 */
+    uint64_t off = a - base;                 /* u64: wraps for a < base (A10) */
+    uint64_t r = off % size;
+    r = r - r % w;                           /* keep the access w-aligned (A3) */
+    return base + r;
+}
+
 int or_check_ok(uint64_t a, uint64_t base, uint64_t size, uint32_t w) {
     /* Every byte of [a, a+w) inside [base, base+size), a w-aligned.         */
     if (a % w != 0) return 0;
@@ -63,6 +72,7 @@ int or_check_range(uint64_t base, uint64_t size, uint64_t addr, uint64_t len) {
 uint64_t or_resolve(const or_ctx *c, uint64_t a, uint32_t w, int *ok) {
     *ok = 1;
     if (c->mode == OR_MASK) return or_fence_mask(a, c->base, c->size, w);
+    if (c->mode == OR_MODULO) return or_fence_modulo(a, c->base, c->size, w);
     if (c->mode == OR_CHECK) {
         if (!or_check_ok(a, c->base, c->size, w)) {
             *ok = 0;
@@ -217,6 +227,8 @@ uint64_t or_desc_rows(const or_ctx *c, uint64_t p, uint64_t rows,
         /* the descriptor's global address is fenced like a 16-byte access
          * (tensor-map addresses must be 16-byte aligned)                   */
         pf = or_fence_mask(p, c->base, c->size, 16);
+    } else if (c->mode == OR_MODULO) {
+        pf = or_fence_modulo(p, c->base, c->size, 16);
     } else {
         /* check: the start must itself be a legal 16-byte-aligned address */
         if (!or_check_ok(p, c->base, c->size, 16)) return 0;
@@ -288,4 +300,8 @@ void or_gemm(or_ctx *c, uint64_t C, uint64_t A, uint64_t B, uint32_t M,
     }
     free(arow);
     free(brow);
+}
+
+void or_fence_modulo_n(const uint64_t *a, uint64_t n, uint64_t base, uint64_t size, uint32_t w, uint64_t *out) {
+    for (uint64_t i = 0; i < n; i++) out[i] = or_fence_modulo(a[i], base, size, w);
 }

@@ -31,7 +31,7 @@ extern "C" {
 /* Fence modes: none = native kernel ("issues a native kernel"),
  * mask = address fencing with bitwise operations,
  * check = address checking.          */
-enum { OR_NONE = 0, OR_MASK = 1, OR_CHECK = 2 };
+enum { OR_NONE = 0, OR_MASK = 1, OR_CHECK = 2, OR_MODULO = 3 };
 
 /* One simulated tenant launch context.
  *   va, len, bytes : the simulated device memory; byte bytes[k] stands for
@@ -66,6 +66,11 @@ uint64_t or_mask(uint64_t size);
  * base (Listing 1 lines 26-28).  The mask additionally clears the low log2(w)
  * bits so a fenced access stays w-aligned.             */
 uint64_t or_fence_mask(uint64_t a, uint64_t base, uint64_t size, uint32_t w);
+/* Modulo-mode fence (§4.4): partition_base +
+ * ((arbitrary_addr - partition_base) % partition_size), with the 64-bit
+ * unsigned remainder (reading A10: a - base wraps mod 2^64 for a < base),
+ * rounded down to a multiple of w (reading A3; size is a multiple of 16).   */
+uint64_t or_fence_modulo(uint64_t a, uint64_t base, uint64_t size, uint32_t w);
 /* Check-mode predicate: the w bytes [a, a+w) all lie in [base, base+size) and
  * a is w-aligned ("partition base and ending addresses";
  * SURVEY.md §8(c) A2, A3).  Returns 1 for an allowed access.                */
@@ -82,6 +87,8 @@ void or_fence_mask_n(const uint64_t *a, uint64_t n, uint64_t base,
                      uint64_t size, uint32_t w, uint64_t *out);
 void or_check_ok_n(const uint64_t *a, uint64_t n, uint64_t base,
                    uint64_t size, uint32_t w, uint8_t *out);
+void or_fence_modulo_n(const uint64_t *a, uint64_t n, uint64_t base,
+                       uint64_t size, uint32_t w, uint64_t *out);
 
 /* ---- simulated kernels -------------------------------- */
 /* copy: 16-byte units, then the byte tail.                                   */

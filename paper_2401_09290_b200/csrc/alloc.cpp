@@ -43,6 +43,32 @@ void Buddy::free(uint64_t off, unsigned order) {
     free_[order].insert(off);
 }
 
+namespace {
+// Split [lo, hi) into maximal aligned power-of-two blocks, ascending.
+template <typename F>
+void aligned_pieces(uint64_t lo, uint64_t hi, unsigned max_order, F f) {
+    while (lo < hi) {
+        unsigned k = lo ? (unsigned)__builtin_ctzll(lo) : max_order;
+        if (k > max_order) k = max_order;
+        while ((1ull << k) > hi - lo) k--;
+        f(lo, k);
+        lo += 1ull << k;
+    }
+}
+}  // namespace
+
+bool Buddy::alloc_exact(uint64_t bytes, uint64_t *off) {
+    unsigned order = min_order_;
+    while ((1ull << order) < bytes) order++;
+    if (order > max_order_ || !alloc(order, off)) return false;
+    aligned_pieces(*off + bytes, *off + (1ull << order), max_order_, [this](uint64_t o, unsigned k) { free(o, k); });
+    return true;
+}
+
+void Buddy::free_exact(uint64_t off, uint64_t bytes) {
+    aligned_pieces(off, off + bytes, max_order_, [this](uint64_t o, unsigned k) { free(o, k); });
+}
+
 uint64_t Buddy::free_bytes() const {
     uint64_t s = 0;
     for (unsigned k = 0; k < free_.size(); k++) s += (uint64_t)free_[k].size() << k;

@@ -261,11 +261,21 @@ extern "C" gd_status gd_arena_info(const gd_arena *a, uint64_t *base, uint64_t *
 // Partitions
 // ===========================================================================
 
-extern "C" gd_status gd_partition_alloc(gd_arena *a, uint64_t requested, gd_partition_info *out) {
-    if (!a || !out || requested == 0 || requested > a->size) return GD_ERR_INVALID_ARG;
-    uint64_t size = GD_MIN_PARTITION;
-    while (size < requested) size <<= 1;                 // next pow2 >= max(req, 4 KiB)
-    std::lock_guard<std::mutex> lk(a->mu);
+namespace {
+
+void fill_info(uint32_t id, const Partition &p, gd_partition_info *out) {
+    out->id = id;
+    out->flags = p.pow2 ? GD_PART_POW2 : 0u;
+    out->base = p.base;
+    out->size = p.size;
+    out->mask = p.size - 1;
+    out->end = p.base + p.size;
+}
+
+// Carve a partition of `size` bytes (pow2: aligned to its size; exact:
+// aligned to next_pow2(size), tail returned to the buddy), back it
+// physically, scrub it, zero its counters.  Caller holds a->mu.
+gd_status carve(gd_arena *a, uint64_t size, bool pow2, gd_partition_info *out) {
     uint32_t id = GD_MAX_TENANTS;
     for (uint32_t i = 0; i < GD_MAX_TENANTS; i++)
         if (!a->parts[i].live) {
@@ -275,13 +285,18 @@ extern "C" gd_status gd_partition_alloc(gd_arena *a, uint64_t requested, gd_part
     if (id == GD_MAX_TENANTS) return GD_ERR_DEVICE_OOM;
     const unsigned order = log2u(size);
     uint64_t off = 0;
-    if (!a->buddy.alloc(order, &off)) return GD_ERR_DEVICE_OOM;
+    const bool got = pow2 ? a->buddy.alloc(order, &off) : a->buddy.alloc_exact(size, &off);
+    if (!got) return GD_ERR_DEVICE_OOM;
+    auto give_back = [&] {
+        if (pow2) a->buddy.free(off, order);
+        else a->buddy.free_exact(off, size);
+    };
     const uint64_t b = a->base + off;
     if (a->device >= 0) {
         DeviceGuard dg(a->device);
         gd_status st = back_partition(a, b, size);
         if (st != GD_OK) {
-            a->buddy.free(off, order);
+            give_back();
             return st;
         }
         // scrub (reading A15) and zero this tenant's counters
@@ -292,7 +307,7 @@ extern "C" gd_status gd_partition_alloc(gd_arena *a, uint64_t requested, gd_part
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
             unback_partition(a, b, size);
-            a->buddy.free(off, order);
+            give_back();
             return cuda_fail(e);
         }
     }
@@ -301,15 +316,30 @@ extern "C" gd_status gd_partition_alloc(gd_arena *a, uint64_t requested, gd_part
     p.base = b;
     p.size = size;
     p.order = order;
+    p.pow2 = pow2;
     p.sub.init(size);
     for (unsigned k = 0; k < GD_NUM_KINDS; k++) a->host[id][k] = HostCounters{};
-    out->id = id;
-    out->reserved = 0;
-    out->base = b;
-    out->size = size;
-    out->mask = size - 1;
-    out->end = b + size;
+    fill_info(id, p, out);
     return GD_OK;
+}
+
+}  // namespace
+
+extern "C" gd_status gd_partition_alloc(gd_arena *a, uint64_t requested, gd_partition_info *out) {
+    if (!a || !out || requested == 0 || requested > a->size) return GD_ERR_INVALID_ARG;
+    uint64_t size = GD_MIN_PARTITION;
+    while (size < requested) size <<= 1;                 // next pow2 >= max(req, 4 KiB)
+    std::lock_guard<std::mutex> lk(a->mu);
+    return carve(a, size, true, out);
+}
+
+extern "C" gd_status gd_partition_alloc_exact(gd_arena *a, uint64_t requested, gd_partition_info *out) {
+    if (!a || !out || requested == 0 || requested > a->size) return GD_ERR_INVALID_ARG;
+    const uint64_t g = a->vmm ? a->gran : GD_MIN_PARTITION;     // physical backing granule
+    uint64_t size = (requested + g - 1) / g * g;
+    if (size < GD_MIN_PARTITION) size = GD_MIN_PARTITION;
+    std::lock_guard<std::mutex> lk(a->mu);
+    return carve(a, size, (size & (size - 1)) == 0, out);
 }
 
 extern "C" gd_status gd_partition_free(gd_arena *a, uint32_t id) {
@@ -322,7 +352,8 @@ extern "C" gd_status gd_partition_free(gd_arena *a, uint32_t id) {
         cudaDeviceSynchronize();                          // no launch may still use it
         unback_partition(a, p.base, p.size);
     }
-    a->buddy.free(p.base - a->base, p.order);
+    if (p.pow2) a->buddy.free(p.base - a->base, p.order);
+    else a->buddy.free_exact(p.base - a->base, p.size);
     p.live = false;
     return GD_OK;
 }
@@ -331,13 +362,7 @@ extern "C" gd_status gd_partition_get(const gd_arena *a, uint32_t id, gd_partiti
     if (!a || !out) return GD_ERR_INVALID_ARG;
     std::lock_guard<std::mutex> lk(const_cast<gd_arena *>(a)->mu);
     if (id >= GD_MAX_TENANTS || !a->parts[id].live) return GD_ERR_UNKNOWN_PARTITION;
-    const Partition &p = a->parts[id];
-    out->id = id;
-    out->reserved = 0;
-    out->base = p.base;
-    out->size = p.size;
-    out->mask = p.size - 1;
-    out->end = p.base + p.size;
+    fill_info(id, a->parts[id], out);
     return GD_OK;
 }
 
@@ -437,10 +462,12 @@ namespace gd {
 // returned before anything is issued.
 gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry) {
     if (!a) return GD_ERR_INVALID_ARG;
-    if (w.mode > GD_MODE_CHECK || w.kind >= GD_NUM_KINDS) return GD_ERR_INVALID_ARG;
+    if (w.mode > GD_MODE_MODULO || w.kind >= GD_NUM_KINDS) return GD_ERR_INVALID_ARG;
     uint64_t base, size;
     gd_status st = snapshot(a, w.tenant, &base, &size);
     if (st != GD_OK) return st;
+    // mask fencing needs a power-of-two, size-aligned partition
+    if (w.mode == GD_MODE_MASK && ((size & (size - 1)) || (base & (size - 1)))) return GD_ERR_NOT_POW2;
 
     uint64_t bytes = 0, flops = 0, t;
     bool empty = false;
@@ -498,6 +525,8 @@ gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry)
     FenceDesc fd;
     fd.base = base;
     fd.mask = size - 1;
+    fd.size = size;
+    fd.inv = recip64(size);
     fd.viol = a->d_stats + (uint64_t)w.tenant * GD_NUM_KINDS + w.kind;
     const Geom g{a->sms};
     DeviceGuard dg(a->device);

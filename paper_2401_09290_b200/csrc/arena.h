@@ -21,6 +21,11 @@ public:
     // returns false when no block of 2^order bytes is free
     bool alloc(unsigned order, uint64_t *off);
     void free(uint64_t off, unsigned order);
+    // Exact-size extent (bytes a multiple of 2^min_order): take the block of
+    // next_pow2(bytes) and give its tail back as aligned sub-blocks; freeing
+    // returns the extent's aligned sub-blocks, which coalesce with the tail.
+    bool alloc_exact(uint64_t bytes, uint64_t *off);
+    void free_exact(uint64_t off, uint64_t bytes);
     uint64_t free_bytes() const;
     unsigned max_order() const { return max_order_; }
     unsigned min_order() const { return min_order_; }
@@ -46,6 +51,7 @@ struct Partition {
     bool live = false;
     uint64_t base = 0, size = 0;
     unsigned order = 0;
+    bool pow2 = true;              // false: exact-size partition (modulo / check / none modes)
     SubAlloc sub;
 };
 

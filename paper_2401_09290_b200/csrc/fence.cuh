@@ -7,15 +7,21 @@
 // paper's "mask and the base partition address" parameters (PAPER.md:175
 // §4.2.3, Listing 1 lines 5-7 and 17-18, reading A12).
 //
-//   MASK : f = (a & mask_w) | base        Listing 1 lines 26-28 (and.b64, or.b64)
-//          mask_w = (size-1) & ~(w-1)      reading A3 (keeps w-alignment)
-//          -> on sm_100 one LOP3 per 32-bit half, operands uniform.
-//   CHECK: ok = ((a - base) & ~mask_w) == 0
-//          <=> a-base in [0, size-w] and a % w == 0 (base is size-aligned)
-//          PAPER.md:175 ("partition base and ending addresses"), 236; A1, A2.
-//          A refused load yields 0, a refused store/atomic is dropped, and
-//          the refusal is counted (aggregated per thread, then per CTA).
-//   NONE : identity (the unfenced twin, "native kernel").
+//   MASK  : f = (a & mask_w) | base        Listing 1 lines 26-28 (and.b64, or.b64)
+//           mask_w = (size-1) & ~(w-1)      reading A3 (keeps w-alignment)
+//           -> on sm_100 one LOP3 per 32-bit half, operands uniform.
+//           Needs a power-of-two, size-aligned partition.
+//   MODULO: f = base + (((a - base) mod size) & ~(w-1))     PAPER.md:238-244 §4.4
+//           the 64-bit modulo inline with the reciprocal parameter
+//           inv = floor(2^64 / size) ("an extra parameter holding the
+//           1/partition_size"): q = mulhi(off, inv) is off/size
+//           or one less, so one conditional subtract finishes it.  Works for
+//           any partition size that is a multiple of 16.
+//   CHECK : ok = (a - base) <= size - w  and  a % w == 0
+//           PAPER.md:175 ("partition base and ending addresses"), 236; A1, A2.
+//           A refused load yields 0, a refused store/atomic is dropped, and
+//           the refusal is counted (aggregated per thread, then per CTA).
+//   NONE  : identity (the unfenced twin, "native kernel").
 #pragma once
 #include <cstdint>
 
@@ -26,17 +32,25 @@ namespace gd {
 // Per-width precomputation, hoisted out of every loop (uniform values).
 template <int MODE, int W>
 struct Fence {
-    uint64_t base, keep;           // keep = mask & ~(W-1)
+    uint64_t base, keep, size, inv, lim;
     __device__ __forceinline__ explicit Fence(const FenceDesc &fd)
-        : base(fd.base), keep(fd.mask & ~(uint64_t)(W - 1)) {}
-    // address the access really uses (MASK: fenced; CHECK/NONE: unchanged)
+        : base(fd.base), keep(fd.mask & ~(uint64_t)(W - 1)), size(fd.size), inv(fd.inv), lim(fd.size - W) {}
+    // address the access really uses (MASK / MODULO: fenced; CHECK / NONE: unchanged)
     __device__ __forceinline__ uint64_t addr(uint64_t a) const {
-        if constexpr (MODE == kMask) return (a & keep) | base;
-        else return a;
+        if constexpr (MODE == kMask) {
+            return (a & keep) | base;
+        } else if constexpr (MODE == kModulo) {
+            const uint64_t off = a - base;
+            uint64_t r = off - __umul64hi(off, inv) * size;
+            if (r >= size) r -= size;
+            return base + (r & ~(uint64_t)(W - 1));
+        } else {
+            return a;
+        }
     }
     // may the access be performed?
     __device__ __forceinline__ bool ok(uint64_t a) const {
-        if constexpr (MODE == kCheck) return ((a - base) & ~keep) == 0;
+        if constexpr (MODE == kCheck) return (a - base) <= lim && (a & (uint64_t)(W - 1)) == 0;
         else return true;
     }
 };
@@ -47,8 +61,8 @@ struct Fence {
 // them) and refuses none, so it may run the unchecked body; only tiles that
 // touch or cross the partition edge pay for per-access checks.
 __device__ __forceinline__ bool range_in(const FenceDesc &fd, uint64_t a, uint64_t len) {
-    const uint64_t size = fd.mask + 1, off = a - fd.base;
-    return len <= size && off <= size - len;
+    const uint64_t off = a - fd.base;
+    return len <= fd.size && off <= fd.size - len;
 }
 
 // Sum a per-thread refusal count over the CTA and add it to the trusted

@@ -4,14 +4,22 @@
 
 namespace gd {
 
-enum Mode : int { kNone = 0, kMask = 1, kCheck = 2 };
+enum Mode : int { kNone = 0, kMask = 1, kCheck = 2, kModulo = 3 };
 
 // Launch-time partition descriptor.  Built on the host
 // from an immutable snapshot of the bounds-table row.
 struct FenceDesc {
-    uint64_t base;                 // partition base, size-aligned
-    uint64_t mask;                 // size - 1
+    uint64_t base;                 // partition base (size-aligned for pow2 partitions)
+    uint64_t mask;                 // size - 1 (the mask-mode fence; pow2 partitions only)
+    uint64_t size;                 // partition size in bytes (check / modulo)
+    uint64_t inv;                  // floor(2^64 / size): modulo-mode reciprocal
     unsigned long long *viol;      // trusted counter (outside every partition)
 };
+
+// floor(2^64 / s) for s >= 2
+inline uint64_t recip64(uint64_t s) {
+    const uint64_t q = ~0ull / s, r = ~0ull % s;
+    return r == s - 1 ? q + 1 : q;
+}
 
 }  // namespace gd

@@ -481,12 +481,13 @@ uint64_t desc_rows(int mode, uint64_t base, uint64_t size, uint64_t p, uint64_t 
                    uint64_t stride, uint64_t *pf) {
     *pf = p;
     if (mode == kNone) return rows;
-    const uint64_t keep = (size - 1) & ~15ull;
     uint64_t f;
     if (mode == kMask) {
-        f = (p & keep) | base;
+        f = (p & ((size - 1) & ~15ull)) | base;
+    } else if (mode == kModulo) {
+        f = base + (((p - base) % size) & ~15ull);
     } else {
-        if (((p - base) & ~keep) != 0) return 0;      // not a legal 16-byte access of the partition
+        if (p - base > size - 16 || (p & 15)) return 0;   // not a legal 16-byte access of the partition
         f = p;
     }
     *pf = f;

@@ -255,6 +255,7 @@ cudaError_t launch_gather(int mode, const FenceDesc &fd, uint64_t out, uint64_t 
     switch (mode) {
         case kNone: return gather_t<kNone>(fd, out, table, idx, n, D, s, g);
         case kMask: return gather_t<kMask>(fd, out, table, idx, n, D, s, g);
+        case kModulo: return gather_t<kModulo>(fd, out, table, idx, n, D, s, g);
         default: return gather_t<kCheck>(fd, out, table, idx, n, D, s, g);
     }
 }
@@ -264,6 +265,7 @@ cudaError_t launch_scatter(int mode, const FenceDesc &fd, uint64_t table, uint64
     switch (mode) {
         case kNone: return scatter_t<kNone>(fd, table, idx, src, n, s);
         case kMask: return scatter_t<kMask>(fd, table, idx, src, n, s);
+        case kModulo: return scatter_t<kModulo>(fd, table, idx, src, n, s);
         default: return scatter_t<kCheck>(fd, table, idx, src, n, s);
     }
 }

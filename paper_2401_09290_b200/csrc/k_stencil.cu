@@ -174,6 +174,7 @@ cudaError_t launch_stencil(int mode, const FenceDesc &fd, uint64_t out, uint64_t
     switch (mode) {
         case kNone: return stencil_t<kNone>(fd, out, in, H, W, pitch, c0, c1, s);
         case kMask: return stencil_t<kMask>(fd, out, in, H, W, pitch, c0, c1, s);
+        case kModulo: return stencil_t<kModulo>(fd, out, in, H, W, pitch, c0, c1, s);
         default: return stencil_t<kCheck>(fd, out, in, H, W, pitch, c0, c1, s);
     }
 }

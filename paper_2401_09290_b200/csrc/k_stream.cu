@@ -197,6 +197,7 @@ cudaError_t launch_copy(int mode, const FenceDesc &fd, uint64_t dst, uint64_t sr
     switch (mode) {
         case kNone: return copy_t<kNone>(fd, dst, src, nbytes, s);
         case kMask: return copy_t<kMask>(fd, dst, src, nbytes, s);
+        case kModulo: return copy_t<kModulo>(fd, dst, src, nbytes, s);
         default: return copy_t<kCheck>(fd, dst, src, nbytes, s);
     }
 }
@@ -206,6 +207,7 @@ cudaError_t launch_saxpy(int mode, const FenceDesc &fd, float alpha, uint64_t x,
     switch (mode) {
         case kNone: return saxpy_t<kNone>(fd, alpha, x, y, n, s);
         case kMask: return saxpy_t<kMask>(fd, alpha, x, y, n, s);
+        case kModulo: return saxpy_t<kModulo>(fd, alpha, x, y, n, s);
         default: return saxpy_t<kCheck>(fd, alpha, x, y, n, s);
     }
 }

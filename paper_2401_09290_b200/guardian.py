@@ -23,7 +23,9 @@ STATUS = ["GD_OK", "GD_ERR_INVALID_ARG", "GD_ERR_NOT_POW2", "GD_ERR_DEVICE_OOM",
 (GD_ERR_INVALID_ARG, GD_ERR_NOT_POW2, GD_ERR_DEVICE_OOM, GD_ERR_PARTITION_OOM, GD_ERR_UNKNOWN_PARTITION,
  GD_ERR_UNKNOWN_ALLOC, GD_ERR_ALIGN, GD_ERR_OOB_RANGE, GD_ERR_UNSUPPORTED, GD_ERR_CUDA) = range(1, 11)
 GD_MODE_NONE, GD_MODE_MASK, GD_MODE_CHECK = 0, 1, 2
-MODES = {"none": GD_MODE_NONE, "mask": GD_MODE_MASK, "check": GD_MODE_CHECK}
+GD_MODE_MODULO = 3
+MODES = {"none": GD_MODE_NONE, "mask": GD_MODE_MASK, "check": GD_MODE_CHECK, "modulo": GD_MODE_MODULO}
+GD_PART_POW2 = 1
 (GD_KIND_COPY, GD_KIND_SAXPY, GD_KIND_GATHER, GD_KIND_SCATTER, GD_KIND_STENCIL, GD_KIND_GEMM) = range(6)
 GD_NUM_KINDS = 6
 GD_MAX_TENANTS = 64
@@ -32,7 +34,7 @@ KIND_NAMES = ["copy", "saxpy", "gather", "scatter", "stencil", "gemm"]
 
 EXPORTED = [
     "gd_arena_create", "gd_arena_wrap", "gd_arena_destroy", "gd_arena_info",
-    "gd_partition_alloc", "gd_partition_free", "gd_partition_get", "gd_malloc", "gd_free",
+    "gd_partition_alloc", "gd_partition_alloc_exact", "gd_partition_free", "gd_partition_get", "gd_malloc", "gd_free",
     "gd_check_range", "gd_memcpy_h2d", "gd_memcpy_d2h", "gd_partition_fill",
     "gd_launch_fenced_copy", "gd_launch_fenced_saxpy", "gd_launch_fenced_gather",
     "gd_launch_fenced_scatter", "gd_launch_fenced_stencil", "gd_launch_fenced_gemm",
@@ -43,7 +45,7 @@ EXPORTED = [
 
 
 class gd_partition_info(ctypes.Structure):
-    _fields_ = [("id", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("base", ctypes.c_uint64),
+    _fields_ = [("id", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("base", ctypes.c_uint64),
                 ("size", ctypes.c_uint64), ("mask", ctypes.c_uint64), ("end", ctypes.c_uint64)]
 
 
@@ -81,6 +83,7 @@ def _load():
         "gd_arena_destroy": [A],
         "gd_arena_info": [A, P(u64), P(u64), P(i32)],
         "gd_partition_alloc": [A, u64, P(gd_partition_info)],
+        "gd_partition_alloc_exact": [A, u64, P(gd_partition_info)],
         "gd_partition_free": [A, u32],
         "gd_partition_get": [A, u32, P(gd_partition_info)],
         "gd_malloc": [A, u32, u64, P(u64)],
@@ -179,6 +182,7 @@ class Partition:
     def __init__(self, info: gd_partition_info):
         self.id, self.base, self.size = info.id, info.base, info.size
         self.mask, self.end = info.mask, info.end
+        self.pow2 = bool(info.flags & GD_PART_POW2)
 
     def __repr__(self):
         return f"Partition(id={self.id}, base={self.base:#x}, size={self.size:#x})"
@@ -228,6 +232,11 @@ class Arena:
         self.close()
 
     # partitions ---------------------------------------------------------
+    def partition_alloc_exact(self, requested: int) -> Partition:
+        info = gd_partition_info()
+        _chk("gd_partition_alloc_exact", _lib.gd_partition_alloc_exact(self._h, requested, ctypes.byref(info)))
+        return Partition(info)
+
     def partition_alloc(self, requested: int) -> Partition:
         info = gd_partition_info()
         _chk("gd_partition_alloc", _lib.gd_partition_alloc(self._h, requested, ctypes.byref(info)))
