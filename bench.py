@@ -281,14 +281,15 @@ def run_gpu(args):
     ms_per_step = ms / args.steps
     value = world * STEP_BYTES_PER_GPU / (ms_per_step / 1e3) / 1e9
 
-    # ---- overhead vs the unfenced twin: interleaved None/Mask/Check ----
-    per_mode = {"none": [], "mask": [], "check": []}
+    # ---- overhead vs the unfenced twin: interleaved None/Mask/Check/Modulo ----
+    modes = ("none", "mask", "check", "modulo")
+    per_mode = {m: [] for m in modes}
     for _ in range(args.reps):
-        for m in ("none", "mask", "check"):
+        for m in modes:
             per_mode[m].append(allreduce([w.time_steps(m, args.steps)])[0] / args.steps)
     med = {m: statistics.median(v) for m, v in per_mode.items()}
     modes_gbs = {m: round(world * STEP_BYTES_PER_GPU / (med[m] / 1e3) / 1e9, 1) for m in med}
-    overhead = {m: round(100.0 * (med[m] / med["none"] - 1.0), 2) for m in ("mask", "check")}
+    overhead = {m: round(100.0 * (med[m] / med["none"] - 1.0), 2) for m in modes[1:]}
 
     # ---- roofline of the dominant kernel (saxpy: 12 B/element) ----
     solo = {}
@@ -298,7 +299,7 @@ def run_gpu(args):
             solo[(kind, m)] = (statistics.mean(d), nbytes)
     sx_ms, sx_bytes = solo[("saxpy", args.mode)]
     achieved = sx_bytes / (sx_ms / 1e3) / 1e9
-    mode_id = {"none": 0, "mask": 1, "check": 2}[args.mode]
+    mode_id = {"none": 0, "mask": 1, "check": 2, "modulo": 3}[args.mode]
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": ncu_traffic(f"k_saxpy<{mode_id}>"),
                 "kernel": f"k_saxpy<{args.mode}>", "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json)",
@@ -448,7 +449,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--mode", default="mask", choices=["none", "mask", "check"])
+    ap.add_argument("--mode", default="mask", choices=["none", "mask", "check", "modulo"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--reps", type=int, default=5, help="interleaved none/mask/check repetitions")
     ap.add_argument("--e2e-steps", type=int, default=2)

@@ -140,8 +140,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__
     const uint64_t r0 = 1ull + (uint64_t)blockIdx.y * kRows;
     const uint64_t r1 = (r0 + kRows < (uint64_t)H - 1) ? r0 + kRows : (uint64_t)H - 1;
     if (c < W && r0 < r1) {
-        if constexpr (MODE == kCheck) {
-            // conservative extents of everything this strip touches
+        if constexpr (MODE == kCheck || MODE == kModulo) {
+            // conservative extents of everything this strip touches; inside the
+            // partition both the check and the modulo fence are the identity
             const uint64_t lo_in = in + 4 * ((r0 - 1) * pitch + c) - (c ? 4 : 0);
             const uint64_t hi_in = in + 4 * (r1 * pitch + c + 5);
             const uint64_t lo_out = out + 4 * (r0 * pitch + c), hi_out = out + 4 * ((r1 - 1) * pitch + c + 4);
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__
                 range_in(fd, lo_out, hi_out - lo_out))
                 strip<kNone, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
             else
-                strip<kCheck, 1>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+                strip<MODE, 1>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
         } else {
             strip<MODE, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
         }

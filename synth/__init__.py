@@ -146,15 +146,18 @@ def bf16_bits_uniform(rng, n: int, lo=-1.0, hi=1.0) -> np.ndarray:
     return (f.view(np.uint32) >> np.uint32(16)).astype(np.uint16)
 
 
-def oob_indices(rng, k: int, part_words: int, lo_word: int, hi_word: int, table_word: int = 0) -> np.ndarray:
+def oob_indices(rng, k: int, part_words: int, lo_word: int, hi_word: int, table_word: int = 0,
+                below: bool = True) -> np.ndarray:
     """k int32 indices j, relative to a table starting ``table_word`` words
     after the partition base, whose raw word offset ``table_word + j`` lies
     OUTSIDE [0, part_words) (another partition, or outside the arena) while
     its residue mod part_words lies in [lo_word, hi_word) -- so a wrapped
     access lands in a region the test keeps free of same-launch writes
-    (race-free).  Half below the base, half above."""
+    (race-free).  Half below the base, half above
+    (below=False: all above, e.g. for non-power-of-two partitions)."""
     w = rng.integers(lo_word, hi_word, k, dtype=np.int64) - table_word      # residue, relative to table
-    below = rng.random(k) < 0.5
+    below_mask = rng.random(k) < 0.5
+    below = below_mask & below
     m_neg = (w + 2**31) // part_words          # largest m with w - m*P >= -2^31
     m_pos = (2**31 - 1 - w) // part_words      # largest m with w + m*P <= 2^31 - 1
     u = rng.random(k)

@@ -1,0 +1,166 @@
+"""GPU parity of modulo fencing (§4.4)
+on exact-size (non-power-of-two) partitions, against the CPU oracle.
+
+The device computes the 64-bit modulo inline from the reciprocal parameter
+floor(2^64/size); the oracle uses the plain u64 remainder.  Layouts keep every
+wrapped access race-free; out-of-partition indices lie above the base so the
+residue is the plain one (reading A10 covers a < base, tested separately)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from paper_2401_09290_b200 import guardian as g
+from tests.gpu_util import download, first_diff, upload
+
+pytestmark = pytest.mark.gpu
+
+MiB = 1 << 20
+EXACT = 14 * MiB                      # 7 VMM granules: not a power of two
+
+
+def _setup(arenas, seed):
+    a = arenas(64 * MiB)
+    parts = [a.partition_alloc_exact(EXACT) for _ in range(3)]
+    for p in parts:
+        assert p.size == EXACT and not p.pow2
+    rng = synth.rng_for(seed)
+    for p in parts:
+        upload(p.base, synth.random_bytes(rng, p.size))
+    return a, parts, rng
+
+
+def _run(a, parts, t, mode, launch, oracle_fn, expect_violations=None):
+    p = parts[t]
+    snap = {q.id: download(q.base, q.size) for q in parts}
+    a.stats_reset()
+    launch(p)
+    st = a.stats(p.id)
+    mem = oracle.Mem(p.base, buf=snap[p.id].copy())
+    c = oracle_fn(mem, p)
+    got = download(p.base, p.size)
+    assert np.array_equal(got, mem.buf), f"{mode}: {first_diff(got, mem.buf)}"
+    for q in parts:
+        if q.id != p.id:
+            assert np.array_equal(download(q.base, q.size), snap[q.id]), "victim modified"
+    assert c.faults == 0 and st["violations"] == c.violations
+    if expect_violations is not None:
+        assert c.violations == expect_violations
+
+
+def test_exact_partitions_layout(arenas):
+    a = arenas(64 * MiB)
+    ps = [a.partition_alloc_exact(EXACT) for _ in range(3)]
+    for x, y in zip(ps, ps[1:]):
+        assert x.end <= y.base or y.end <= x.base
+    with pytest.raises(g.GuardianError) as e:
+        a.copy(ps[0].id, "mask", ps[0].base, ps[0].base + 16, 64)
+    assert e.value.status == g.GD_ERR_NOT_POW2
+    a.partition_free(ps[1].id)
+    q = a.partition_alloc(16 * MiB)                 # the freed block and its tail coalesced
+    assert q.base % q.size == 0
+
+
+@pytest.mark.parametrize("mode", ["modulo", "check", "none"])
+def test_modulo_copy_crossing_end(arenas, mode):
+    a, parts, _ = _setup(arenas, 601)
+    n = 3 * MiB + 16 * 9 + 5
+    p = parts[1]
+    if mode == "none":                                            # in bounds, ending 11 bytes before end
+        dst = p.end - (n + 11)
+    else:                                                         # the last 512 KiB + 5 bytes cross end
+        dst = p.end - (n - (512 * 1024 + 5))
+    _run(a, parts, 1, mode,
+         lambda p: a.copy(p.id, mode, dst, p.base + 4 * MiB, n),
+         lambda m, p: oracle.copy(m, p.base, p.size, mode, dst, p.base + 4 * MiB, n))
+
+
+@pytest.mark.parametrize("mode", ["modulo", "check"])
+def test_modulo_saxpy_crossing_end(arenas, mode):
+    a, parts, rng = _setup(arenas, 602)
+    n, over = (1 << 19) + 3, (1 << 15) + 3
+    p = parts[0]
+    upload(p.base + 4 * MiB, synth.uniform_f32(rng, n))
+    y = p.end - 4 * (n - over)
+    upload(y, synth.uniform_f32(rng, n - over))
+    upload(p.base, synth.uniform_f32(rng, over))
+    _run(a, parts, 0, mode,
+         lambda p: a.saxpy(p.id, mode, 0.625, p.base + 4 * MiB, y, n),
+         lambda m, p: oracle.saxpy(m, p.base, p.size, mode, 0.625, p.base + 4 * MiB, y, n),
+         None if mode == "modulo" else 2 * over)
+
+
+@pytest.mark.parametrize("mode", ["modulo", "check"])
+def test_modulo_gather_scatter_adversarial(arenas, mode):
+    a, parts, rng = _setup(arenas, 603)
+    p = parts[2]
+    T, n = 1 << 20, (1 << 17) + 3
+    j = rng.integers(0, T, n, dtype=np.int64).astype(np.int32)
+    k = synth.planted_count(0.02, n)
+    pos = synth.planted_positions(rng, n, k)
+    j[pos] = synth.oob_indices(rng, k, EXACT // 4, (10 * MiB) // 4, EXACT // 4, below=False)
+    upload(p.base + 4 * MiB, j)
+    _run(a, parts, 2, mode,
+         lambda p: a.gather(p.id, mode, p.base + 6 * MiB, p.base, p.base + 4 * MiB, n),
+         lambda m, p: oracle.gather(m, p.base, p.size, mode, p.base + 6 * MiB, p.base, p.base + 4 * MiB, n),
+         None if mode == "modulo" else k)
+    _run(a, parts, 2, mode,
+         lambda p: a.scatter(p.id, mode, p.base, p.base + 4 * MiB, p.base + 6 * MiB, n),
+         lambda m, p: oracle.scatter_add(m, p.base, p.size, mode, p.base, p.base + 4 * MiB, p.base + 6 * MiB, n),
+         None if mode == "modulo" else k)
+
+
+@pytest.mark.parametrize("mode", ["modulo", "check"])
+def test_modulo_stencil_out_crossing_end(arenas, mode):
+    a, parts, rng = _setup(arenas, 604)
+    H, W, pitch = 160, 1000, 1024
+    p = parts[1]
+    upload(p.base + 4 * MiB, synth.uniform_f32(rng, H * pitch, 0.0, 1.0))
+    out = p.end - (H - 7) * pitch * 4
+    _run(a, parts, 1, mode,
+         lambda p: a.stencil(p.id, mode, out, p.base + 4 * MiB, H, W, pitch, 0.5, 0.125),
+         lambda m, p: oracle.stencil(m, p.base, p.size, mode, out, p.base + 4 * MiB, H, W, pitch, 0.5, 0.125),
+         None if mode == "modulo" else 6 * (W - 2))
+
+
+@pytest.mark.parametrize("mode", ["modulo", "check"])
+def test_modulo_gemm_A_past_end(arenas, mode):
+    a, parts, rng = _setup(arenas, 605)
+    p = parts[0]
+    M, N, K = 256, 256, 128
+    pa = p.end - (M - 32) * K * 2
+    upload(pa, synth.bf16_bits_uniform(rng, (M - 32) * K))
+    upload(p.base, synth.bf16_bits_uniform(rng, N * K))
+    pc = p.base + 2 * MiB
+    before = download(p.base, p.size)
+    a.stats_reset()
+    a.gemm(p.id, mode, pc, pa, p.base, M, N, K, K, K, N)
+    assert a.device_flags() == 0
+    got = download(p.base, p.size)
+    mem = oracle.Mem(p.base, buf=before)
+    c = oracle.gemm(mem, p.base, p.size, mode, pc, pa, p.base, M, N, K, K, K, N)
+    assert a.stats(p.id)["violations"] == c.violations == (32 if mode == "check" else 0)
+    cm = np.zeros(p.size, bool)
+    cm[2 * MiB:2 * MiB + 2 * M * N] = True
+    assert np.array_equal(got[~cm], mem.buf[~cm])
+    gg = (got[cm].view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    rr = (mem.buf[cm].view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    assert np.linalg.norm(gg - rr) / np.linalg.norm(rr) <= 1e-2
+    assert (got[cm].view(np.uint16).reshape(M, N)[M - 32:] == 0).all()
+
+
+def test_modulo_equals_mask_on_pow2_partition(arenas):
+    """On a power-of-two partition the two fencing methods are the same
+    function: identical results for adversarial indices (incl. j < 0)."""
+    a = arenas(64 * MiB)
+    p = a.partition_alloc(16 * MiB)
+    rng = synth.rng_for(606)
+    upload(p.base, synth.random_bytes(rng, p.size))
+    n = 1 << 16
+    j = synth.oob_indices(rng, n, p.size // 4, (10 * MiB) // 4, p.size // 4)
+    upload(p.base + 4 * MiB, j)
+    outs = []
+    for mode in ("mask", "modulo"):
+        a.gather(p.id, mode, p.base + 6 * MiB, p.base, p.base + 4 * MiB, n)
+        outs.append(download(p.base + 6 * MiB, 4 * n))
+    assert np.array_equal(outs[0], outs[1])

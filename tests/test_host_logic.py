@@ -253,3 +253,62 @@ def test_launcher_validates_all_before_issuing():
         a.launcher_run(items, [None])
     assert e.value.status == g.GD_ERR_ALIGN
     assert a.stats(p.id)["launches"] == 0
+
+
+def test_exact_partitions_tail_returns_to_pool():
+    """gd_partition_alloc_exact: a 12 KiB request takes a
+    16 KiB block and gives the 4 KiB tail back, which a later 4 KiB request
+    receives; freeing coalesces everything back to one block."""
+    a = virtual(1 << 20)
+    x = a.partition_alloc_exact(12 << 10)
+    assert x.size == 12 << 10 and not x.pow2 and x.base == DEV_BASE
+    y = a.partition_alloc(4 << 10)
+    assert y.base == DEV_BASE + (12 << 10)              # the returned tail
+    with pytest.raises(g.GuardianError) as e:
+        a.copy(x.id, "mask", x.base, x.base + 16, 64)
+    assert e.value.status == g.GD_ERR_NOT_POW2
+    with pytest.raises(g.GuardianError) as e:           # modulo / check accepted (no device)
+        a.copy(x.id, "modulo", x.base, x.base + 16, 64)
+    assert e.value.status == g.GD_ERR_UNSUPPORTED
+    a.partition_free(x.id)
+    a.partition_free(y.id)
+    z = a.partition_alloc(1 << 20)                      # fully coalesced again
+    assert z.base == DEV_BASE
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_mixed_exact_and_pow2_fuzz_against_bitmap(seed):
+    """Exact and power-of-two partitions mixed: disjoint, inside the arena,
+    pow2 ones size-aligned, exact ones 4 KiB-aligned and sized; all space
+    comes back after freeing everything."""
+    size = 1 << 24
+    a = virtual(size)
+    ref = BitmapArena(DEV_BASE, size)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    live = {}
+    for _ in range(800):
+        if live and (rng.random() < 0.45 or len(live) >= 60):
+            pid = int(rng.choice(list(live)))
+            a.partition_free(pid)
+            b, s = live.pop(pid)
+            lo = (b - DEV_BASE) // 4096
+            ref.used[lo:lo + s // 4096] = False
+        else:
+            req = int(2 ** rng.uniform(0, 22))
+            exact = rng.random() < 0.5
+            try:
+                p = a.partition_alloc_exact(req) if exact else a.partition_alloc(req)
+            except g.GuardianError as e:
+                assert e.status == g.GD_ERR_DEVICE_OOM
+                continue
+            if exact:
+                assert p.size == max(4096, -(-req // 4096) * 4096) and p.base % 4096 == 0
+            else:
+                assert p.size == partition_size(req) and p.base % p.size == 0
+            lo = (p.base - DEV_BASE) // 4096
+            assert not ref.used[lo:lo + p.size // 4096].any() and p.base + p.size <= DEV_BASE + size
+            ref.used[lo:lo + p.size // 4096] = True
+            live[p.id] = (p.base, p.size)
+    for pid in list(live):
+        a.partition_free(pid)
+    assert a.partition_alloc(size).base == DEV_BASE

@@ -43,7 +43,7 @@ def time_modes(launch, reps, warm=3, extra=None):
     """launch(mode, stream) -> None; interleaved none/mask/check (+ extra
     reference launches {name: fn(stream)} timed in the same rotation)."""
     s = torch.cuda.Stream()
-    res = {m: [] for m in ("none", "mask", "check")}
+    res = {m: [] for m in ("none", "mask", "check", "modulo")}
     extra = extra or {}
     res.update({k: [] for k in extra})
 
@@ -75,7 +75,7 @@ def summarize(name, res, work, unit, peak):
         rate = work / (med / 1e3) / (1e9 if unit == "GB/s" else 1e12)
         out[m] = {"ms_median": round(med, 4), "ms_paper_mean": round(paper_mean(xs), 4), unit: round(rate, 1),
                   "frac_of_peak": round(rate / peak, 4)}
-    for m in ("mask", "check"):
+    for m in ("mask", "check", "modulo"):
         out[m]["overhead_pct"] = round(100 * (out[m]["ms_median"] / out["none"]["ms_median"] - 1), 2)
     print(f"{name:28s} " + "  ".join(f"{m}: {out[m][unit]:8.1f} {unit}" + (f" ({out[m]['overhead_pct']:+.2f}%)"
                                                                            if m != 'none' else '')
