@@ -68,6 +68,27 @@ def time_modes(launch, reps, warm=3, extra=None):
     return res
 
 
+def time_modes_batched(launch, reps, batch=50, warm=3):
+    """L2-resident regime: kernels of a few microseconds are timed as a batch
+    of back-to-back launches between two events (per-launch mean)."""
+    s = torch.cuda.Stream()
+    res = {m: [] for m in ("none", "mask", "check", "modulo")}
+    with torch.cuda.stream(s):
+        for m in res:
+            for _ in range(warm):
+                launch(m, s)
+        for _ in range(reps):
+            for m in res:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                for _ in range(batch):
+                    launch(m, s)
+                b.record(s)
+                b.synchronize()
+                res[m].append(a.elapsed_time(b) / batch)
+    return res
+
+
 def summarize(name, res, work, unit, peak):
     out = {}
     for m, xs in res.items():
@@ -153,6 +174,30 @@ def main():
         r = time_modes(lambda m, s: arena.stencil(p.id, m, b + 8 * GiB, b + 4 * GiB, H, W, W, 0.5, 0.125, stream=s),
                        args.reps)
         results["stencil_32768^2"] = summarize("stencil 32768^2", r, 8 * (H - 2) * (W - 2), "GB/s", hbm)
+
+    if only is not None and "l2" in only:
+        # L2-resident working sets (< 126 MB L2), where the
+        # fence's ALU cost is least hidden (the paper's all-cache-hit worst case,
+        # 28-57 % at 100 % L1 hits)
+        MiB = 1 << 20
+        devmem.view(b, 16 * MiB, torch.int32).random_(generator=gen)
+        r = time_modes_batched(lambda m, s: arena.copy(p.id, m, b + 64 * MiB, b, 32 * MiB, stream=s), args.reps)
+        results["l2_copy_32MiB"] = summarize("L2 copy 32 MiB", r, 2 * 32 * MiB, "GB/s", hbm)
+        devmem.view(b + 128 * MiB, 8 * MiB, torch.float32).uniform_(-1, 1, generator=gen)
+        devmem.view(b + 192 * MiB, 8 * MiB, torch.float32).uniform_(-1, 1, generator=gen)
+        r = time_modes_batched(lambda m, s: arena.saxpy(p.id, m, 1.0, b + 128 * MiB, b + 192 * MiB, 8 * MiB,
+                                                        stream=s), args.reps)
+        results["l2_saxpy_8M"] = summarize("L2 saxpy 2^23", r, 12 * 8 * MiB, "GB/s", hbm)
+        n, T = 1 << 22, 1 << 22                      # 16 MiB table, 16 MiB indices: L2-resident
+        devmem.view(b + 256 * MiB, n, torch.int32).random_(0, T, generator=gen)
+        r = time_modes_batched(lambda m, s: arena.gather(p.id, m, b + 320 * MiB, b, b + 256 * MiB, n, stream=s),
+                               args.reps)
+        results["l2_gather_4M"] = summarize("L2 gather 2^22 into 2^22", r, 12 * n, "GB/s", hbm)
+        H = W = 2048                                 # 16 MiB in + out
+        devmem.view(b + 384 * MiB, H * W, torch.float32).uniform_(0, 1, generator=gen)
+        r = time_modes_batched(lambda m, s: arena.stencil(p.id, m, b + 448 * MiB, b + 384 * MiB, H, W, W, 0.5, 0.125,
+                                                          stream=s), args.reps)
+        results["l2_stencil_2048^2"] = summarize("L2 stencil 2048^2", r, 8 * (H - 2) * (W - 2), "GB/s", hbm)
 
     if want("gemm"):
         n = 8192
