@@ -134,11 +134,11 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                          uint64_t in, uint32_t H, uint32_t W, uint64_t pitch,
-                                                         float c0, float c1) {
+                                                         float c0, float c1, uint32_t rows) {
     uint32_t nv = 0;
     const uint64_t c = 4ull * ((uint64_t)blockIdx.x * kThreads + threadIdx.x);
-    const uint64_t r0 = 1ull + (uint64_t)blockIdx.y * kRows;
-    const uint64_t r1 = (r0 + kRows < (uint64_t)H - 1) ? r0 + kRows : (uint64_t)H - 1;
+    const uint64_t r0 = 1ull + (uint64_t)blockIdx.y * rows;
+    const uint64_t r1 = (r0 + rows < (uint64_t)H - 1) ? r0 + rows : (uint64_t)H - 1;
     if (c < W && r0 < r1) {
         if constexpr (MODE == kCheck || MODE == kModulo) {
             // conservative extents of everything this strip touches; inside the
@@ -160,23 +160,27 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__
 
 template <int MODE>
 cudaError_t stencil_t(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t H, uint32_t W, uint64_t pitch,
-                      float c0, float c1, cudaStream_t s) {
-    const uint64_t nvec = (W + 3ull) / 4;
-    const dim3 grid((unsigned)((nvec + kThreads - 1) / kThreads), (unsigned)((H - 2ull + kRows - 1) / kRows));
-    k_stencil<MODE><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
+                      float c0, float c1, cudaStream_t s, int sms) {
+    const uint64_t nvec = (W + 3ull) / 4, gx = (nvec + kThreads - 1) / kThreads;
+    // rows per CTA strip: long strips amortise the 2-row halo; small grids
+    // (L2-resident sizes) get short strips so that every SM has 4 CTAs
+    uint32_t rows = kRows;
+    while (rows > 4 && gx * ((H - 2ull + rows - 1) / rows) < 4ull * (uint64_t)sms) rows /= 2;
+    const dim3 grid((unsigned)gx, (unsigned)((H - 2ull + rows - 1) / rows));
+    k_stencil<MODE><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1, rows);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_stencil(int mode, const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t H, uint32_t W,
-                           uint64_t pitch, float c0, float c1, cudaStream_t s, const Geom &) {
+                           uint64_t pitch, float c0, float c1, cudaStream_t s, const Geom &g) {
     if (H < 3 || W < 3) return cudaSuccess;        // no interior point
     switch (mode) {
-        case kNone: return stencil_t<kNone>(fd, out, in, H, W, pitch, c0, c1, s);
-        case kMask: return stencil_t<kMask>(fd, out, in, H, W, pitch, c0, c1, s);
-        case kModulo: return stencil_t<kModulo>(fd, out, in, H, W, pitch, c0, c1, s);
-        default: return stencil_t<kCheck>(fd, out, in, H, W, pitch, c0, c1, s);
+        case kNone: return stencil_t<kNone>(fd, out, in, H, W, pitch, c0, c1, s, g.sms);
+        case kMask: return stencil_t<kMask>(fd, out, in, H, W, pitch, c0, c1, s, g.sms);
+        case kModulo: return stencil_t<kModulo>(fd, out, in, H, W, pitch, c0, c1, s, g.sms);
+        default: return stencil_t<kCheck>(fd, out, in, H, W, pitch, c0, c1, s, g.sms);
     }
 }
 

@@ -1,0 +1,90 @@
+"""GPU checks of the C ABI around the kernels: checked host transfers
+(§4.2.2), scrubbing on (re)allocation (reading A15), the
+trusted counters' placement outside the arena, per-kind stats,
+and the partition fill used for the address-revealing pattern."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from paper_2401_09290_b200 import guardian as g
+from tests.gpu_util import download, upload
+
+pytestmark = pytest.mark.gpu
+MiB = 1 << 20
+
+
+def test_checked_transfers(arenas):
+    a = arenas(4 * MiB)
+    p, q = a.partition_alloc(MiB), a.partition_alloc(MiB)
+    host = torch.arange(65536, dtype=torch.int32).pin_memory()
+    a.memcpy_h2d(p.id, p.base + 4096, host.data_ptr(), 4 * 65536)
+    torch.cuda.synchronize()
+    assert np.array_equal(download(p.base + 4096, 4 * 65536).view(np.int32), np.arange(65536, dtype=np.int32))
+    back = torch.zeros(65536, dtype=torch.int32).pin_memory()
+    a.memcpy_d2h(p.id, back.data_ptr(), p.base + 4096, 4 * 65536)
+    torch.cuda.synchronize()
+    assert torch.equal(back, host)
+    qbefore = download(q.base, q.size)
+    for dst, n in ((p.end - 8, 16), (q.base, 16), (p.base - 4, 8), (2**64 - 8, 16)):
+        with pytest.raises(g.GuardianError) as e:
+            a.memcpy_h2d(p.id, dst, host.data_ptr(), n)
+        assert e.value.status == g.GD_ERR_OOB_RANGE
+    with pytest.raises(g.GuardianError) as e:
+        a.memcpy_d2h(p.id, back.data_ptr(), q.base, 64)          # reading the neighbour is refused too
+    assert e.value.status == g.GD_ERR_OOB_RANGE
+    assert np.array_equal(download(q.base, q.size), qbefore)
+    a.memcpy_h2d(p.id, p.end - 16, host.data_ptr(), 16)          # ending exactly at end is fine
+
+
+def test_partitions_are_scrubbed_on_reuse(arenas):
+    a = arenas(4 * MiB)
+    p = a.partition_alloc(MiB)
+    upload(p.base, synth.random_bytes(synth.rng_for(1), MiB))
+    a.partition_free(p.id)
+    q = a.partition_alloc(MiB)
+    assert q.base == p.base
+    assert not download(q.base, q.size).any()                    # no leak from the previous tenant
+
+
+def test_stats_live_outside_arena_and_count_per_kind(arenas):
+    a = arenas(4 * MiB)
+    p = a.partition_alloc(MiB)
+    sp = a.stats_device_ptr()
+    assert sp + 8 * g.GD_MAX_TENANTS * g.GD_NUM_KINDS <= a.base or sp >= a.base + a.size
+    a.stats_reset()
+    a.copy(p.id, "check", p.base, p.base + MiB, 64)                # src outside: 4 refused loads
+    a.gather(p.id, "check", p.base + 4096, p.base, p.base + 8192, 4)
+    st = a.stats(p.id)
+    assert st["violations_by_kind"]["copy"] == 4
+    assert st["launches_by_kind"]["copy"] == 1 and st["launches_by_kind"]["gather"] == 1
+    assert st["bytes"] == 2 * 64 + (4 + 8) * 4
+    a.stats_reset(p.id)
+    assert a.stats(p.id)["violations"] == 0
+
+
+def test_partition_fill_pattern(arenas):
+    a = arenas(4 * MiB)
+    p = a.partition_alloc(MiB)
+    a.fill(p.id, 1, 4096, 65536)
+    got = download(p.base + 4096, 65536).view(np.uint32)
+    np.testing.assert_array_equal(got, synth.pattern_words(np.arange(4096, 4096 + 65536, 4, dtype=np.uint64)))
+    with pytest.raises(g.GuardianError) as e:
+        a.fill(p.id, 1, MiB - 16, 32)
+    assert e.value.status == g.GD_ERR_OOB_RANGE
+
+
+def test_streams_from_torch_and_async(arenas):
+    """Launches are asynchronous on the caller's torch stream."""
+    a = arenas(64 * MiB)
+    p = a.partition_alloc(32 * MiB)
+    s = torch.cuda.Stream()
+    upload(p.base, synth.random_bytes(synth.rng_for(2), 8 * MiB))
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        a.copy(p.id, "mask", p.base + 16 * MiB, p.base, 8 * MiB, stream=s)
+    s.synchronize()
+    assert np.array_equal(download(p.base + 16 * MiB, 8 * MiB), download(p.base, 8 * MiB))
+    assert a.device_flags() == 0

@@ -1,0 +1,73 @@
+"""Isolation properties on the GPU (§5: a kernel cannot
+access memory outside its partition).
+
+* No foreign reads: every partition is filled with words tagged by their
+  owner; an adversarial tenant gathers and copies through arbitrary int32
+  indices and raw pointers in mask / modulo mode -- every value it obtains
+  carries its own tag, and every other partition is unchanged.
+* compute-sanitizer memcheck: the fenced adversarial run performs no invalid
+  access at all; the unfenced twin does (run in a subprocess, since an
+  unfenced out-of-range access can kill the shared context)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from paper_2401_09290_b200 import devmem
+from tests.gpu_util import download
+
+pytestmark = pytest.mark.gpu
+MiB = 1 << 20
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("mode", ["mask", "modulo"])
+def test_no_foreign_reads(arenas, mode):
+    a = arenas(4 * 16 * MiB)
+    parts = [a.partition_alloc(16 * MiB) for _ in range(4)]
+    for t, p in enumerate(parts):
+        w = p.size // 4
+        tag = torch.arange(w, dtype=torch.int64, device="cuda") & 0x0FFFFFFF | (t << 28)
+        devmem.view(p.base, w, torch.int32).copy_(tag.to(torch.int32))
+    torch.cuda.synchronize()
+    snaps = [download(q.base, q.size) for q in parts]
+    p = parts[2]
+    rng = synth.rng_for(901)
+    n = 1 << 18
+    j = synth.chaos_indices(rng, n)
+    devmem.view(p.base + 4 * MiB, n, torch.int32).copy_(torch.from_numpy(j))
+    a.gather(p.id, mode, p.base + 6 * MiB, p.base, p.base + 4 * MiB, n)
+    out = download(p.base + 6 * MiB, 4 * n).view(np.uint32)
+    assert ((out >> 28) == 2).all(), "a gathered value came from another partition"
+    for src in (parts[0].base, parts[3].base + 12345 * 16, 0x1000, int(rng.integers(1 << 40, 1 << 47)) & ~15):
+        a.copy(p.id, mode, p.base + 8 * MiB, src, 256 * 1024)
+        got = download(p.base + 8 * MiB, 256 * 1024).view(np.uint32)
+        assert ((got >> 28) == 2).all(), hex(src)
+    for t, q in enumerate(parts):
+        if t != 2:
+            assert np.array_equal(download(q.base, q.size), snaps[t]), f"partition {t} modified"
+
+
+def _sanitize(mode):
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    cmd = [exe, "--tool", "memcheck", "--error-exitcode", "9", sys.executable,
+           os.path.join(ROOT, "tools", "adversarial.py"), "--mode", mode]
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+
+
+@pytest.mark.parametrize("mode", ["mask", "modulo", "check"])
+def test_sanitizer_clean_when_fenced(mode):
+    r = _sanitize(mode)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr
+
+
+def test_sanitizer_flags_unfenced_twin():
+    r = _sanitize("none")
+    assert r.returncode != 0
+    assert "Invalid __global__" in r.stdout + r.stderr or "ERROR SUMMARY: 0 errors" not in r.stdout + r.stderr
