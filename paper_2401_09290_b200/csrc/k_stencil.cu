@@ -131,10 +131,15 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
     }
 }
 
-template <int MODE>
+// ROWS (rows per CTA strip) is a compile-time constant: long strips (64)
+// amortise the 2-row halo at HBM sizes, short ones (8) keep every SM busy at
+// L2-resident sizes; as a constant it also keeps the check / modulo variants
+// (hoisted body + per-access body) inside 64 registers with no local memory.
+template <int MODE, int ROWS>
 __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                          uint64_t in, uint32_t H, uint32_t W, uint64_t pitch,
-                                                         float c0, float c1, uint32_t rows) {
+                                                         float c0, float c1) {
+    constexpr uint64_t rows = ROWS;
     uint32_t nv = 0;
     const uint64_t c = 4ull * ((uint64_t)blockIdx.x * kThreads + threadIdx.x);
     const uint64_t r0 = 1ull + (uint64_t)blockIdx.y * rows;
@@ -162,12 +167,14 @@ template <int MODE>
 cudaError_t stencil_t(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t H, uint32_t W, uint64_t pitch,
                       float c0, float c1, cudaStream_t s, int sms) {
     const uint64_t nvec = (W + 3ull) / 4, gx = (nvec + kThreads - 1) / kThreads;
-    // rows per CTA strip: long strips amortise the 2-row halo; small grids
-    // (L2-resident sizes) get short strips so that every SM has 4 CTAs
-    uint32_t rows = kRows;
-    while (rows > 4 && gx * ((H - 2ull + rows - 1) / rows) < 4ull * (uint64_t)sms) rows /= 2;
-    const dim3 grid((unsigned)gx, (unsigned)((H - 2ull + rows - 1) / rows));
-    k_stencil<MODE><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1, rows);
+    // long strips unless that leaves fewer than 4 CTAs per SM
+    if (gx * ((H - 2ull + kRows - 1) / kRows) >= 4ull * (uint64_t)sms) {
+        const dim3 grid((unsigned)gx, (unsigned)((H - 2ull + kRows - 1) / kRows));
+        k_stencil<MODE, kRows><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
+    } else {
+        const dim3 grid((unsigned)gx, (unsigned)((H - 2ull + 7) / 8));
+        k_stencil<MODE, 8><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
+    }
     return cudaGetLastError();
 }
 
