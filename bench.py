@@ -71,7 +71,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -214,6 +214,57 @@ class Workload:
         else:
             self.arena.saxpy(p.id, mode, ALPHA, p.base + OFF_X, p.base + OFF_Y, SAXPY_N, stream=s)
 
+    def c5(self, launches=20, mode="check", seed_base=5000):
+        """BASELINE.json configs[4] on this GPU: t0-t2 fenced copy (4 GiB),
+        t3-t5 fenced gather (C3: 2^26 indices, 1 % planted OOB), t6-t7 fenced
+        GEMM 8192^3, `launches` launches each, issued round-robin by the
+        launcher on 8 streams.  Returns (makespan ms, bytes, flops, planted)."""
+        import numpy as np
+        import synth
+        torch, g, devmem = self.torch, self.g, self.devmem
+        n_idx, table_n, n = 1 << 26, 1 << 29, 8192
+        items, planted, nbytes, flops = [], 0, 0, 0
+        for t, p in enumerate(self.parts):
+            b = p.base
+            if t < 3:
+                items.append(g.work(p.id, g.GD_KIND_COPY, mode, ptr=(b + OFF_DST, b + OFF_SRC), u64=(COPY_BYTES,)))
+                nbytes += BYTES_COPY
+            elif t < 6:
+                idx, pos = synth.indices_with_oob(synth.rng_for(seed_base + t), n_idx, table_n, 0.01)
+                devmem.view(b + 2 * GiB, n_idx, torch.int32, self.device).copy_(torch.from_numpy(idx))
+                planted += len(pos)
+                items.append(g.work(p.id, g.GD_KIND_GATHER, mode, ptr=(b + 2 * GiB + GiB // 4, b, b + 2 * GiB),
+                                    u64=(n_idx,), u32=(1,)))
+                nbytes += 12 * n_idx
+            else:
+                gen = torch.Generator(device=f"cuda:{self.device}")
+                gen.manual_seed(seed_base + t)
+                for off in (0, n * n * 2):
+                    devmem.view(b + off, n * n, torch.bfloat16, self.device).uniform_(-1, 1, generator=gen)
+                items.append(g.work(p.id, g.GD_KIND_GEMM, mode, ptr=(b + 2 * n * n * 2, b, b + n * n * 2),
+                                    u64=(n, n, n), u32=(n, n, n)))
+                flops += 2 * n ** 3
+        torch.cuda.synchronize(self.device)
+        queue = [it for it in items for _ in range(launches)]
+        self.step(queue[:len(items)])                                     # warm-up round
+        torch.cuda.synchronize(self.device)
+        self.arena.stats_reset()
+        root = torch.cuda.current_stream(self.device)
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize(self.device)
+        start.record(root)
+        for s in self.streams:
+            s.wait_event(start)
+        self.step(queue)
+        for s in self.streams:
+            e = torch.cuda.Event()
+            e.record(s)
+            root.wait_event(e)
+        stop.record(root)
+        torch.cuda.synchronize(self.device)
+        return start.elapsed_time(stop), nbytes * launches, flops * launches, planted * launches
+
     def e2e(self, mode, steps, warmup):
         """Through the public API with HOST buffers: every step copies each
         tenant's inputs host->device (checked transfers, gd_memcpy_h2d), runs
@@ -316,11 +367,27 @@ def run_gpu(args):
                "h2d_bytes_per_step": world * h2d, "d2h_bytes_per_step": world * d2h,
                "steps": args.e2e_steps, "note": "pinned host buffers, checked gd_memcpy_h2d/d2h, PCIe-bound"}
 
+    # ---- C5: mixed tenants (copy / gather 1 % OOB / GEMM) in check mode ----
+    c5 = None
+    c5_expected = 0
+    if not args.no_c5:
+        c5_ms, c5_bytes, c5_flops, c5_planted = w.c5(launches=args.c5_launches)
+        c5_ms_max = allreduce([c5_ms])[0]
+        c5_expected = int(allreduce([float(c5_planted)], op="sum")[0])
+        c5 = {"makespan_ms": round(c5_ms_max, 3), "launches_per_tenant": args.c5_launches, "mode": "check",
+              "memory_GBps": round(world * c5_bytes / (c5_ms_max / 1e3) / 1e9, 1),
+              "gemm_TFLOPs": round(world * c5_flops / (c5_ms_max / 1e3) / 1e12, 1),
+              "tenants": "t0-2 copy 4 GiB, t3-5 gather 2^26 (1% OOB), t6-7 GEMM 8192^3 bf16"}
+
     # ---- statistics reduced over GPUs with NCCL (the one collective) ----
     from paper_2401_09290_b200 import dist as gdist
     per = {rank * TENANTS + t: w.arena.stats(p.id) for t, p in enumerate(w.parts)}
     red_t, span = gdist.allreduce_stats(per, ms, world * TENANTS)
     red = [sum(d[f] for d in red_t.values()) for f in ("violations", "launches", "bytes")]
+    if c5 is not None:
+        c5["violations_allreduced"] = int(red[0])
+        c5["violations_expected"] = c5_expected                       # 3 x 671,089 x launches x G
+        c5["violations_exact"] = int(red[0]) == c5_expected
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -342,6 +409,7 @@ def run_gpu(args):
             "e2e": e2e, "gpu_launches": args.steps * 2 * TENANTS,
             "clocks": clk.summary(),
             "stats_allreduced": {"violations": int(red[0]), "launches": int(red[1]), "bytes": int(red[2])},
+            "multi_tenant_c5": c5,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -455,6 +523,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the mixed multi-tenant (configs[4]) measurement")
+    ap.add_argument("--c5-launches", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -93,10 +93,11 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 }
 
 // grouped raster: tiles t = 0..tm*tn-1 -> (m_blk, n_blk)
-__device__ __forceinline__ void tile_coords(uint32_t t, uint32_t tm, uint32_t tn, uint32_t &mb, uint32_t &nb) {
-    const uint32_t per_group = GROUP_M * tn;
-    const uint32_t g = t / per_group, first = g * GROUP_M;
-    const uint32_t gm = (tm - first < GROUP_M) ? tm - first : GROUP_M;
+__device__ __forceinline__ void tile_coords(uint32_t t, uint32_t tm, uint32_t tn, uint32_t group, uint32_t &mb,
+                                            uint32_t &nb) {
+    const uint32_t per_group = group * tn;
+    const uint32_t g = t / per_group, first = g * group;
+    const uint32_t gm = (tm - first < group) ? tm - first : group;
     const uint32_t r = t - g * per_group;
     mb = first + r % gm;
     nb = r / gm;
@@ -104,7 +105,7 @@ __device__ __forceinline__ void tile_coords(uint32_t t, uint32_t tm, uint32_t tn
 
 __global__ void __launch_bounds__(THREADS, 1)
 k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, uint64_t C, uint64_t ldc,
-       uint32_t N, uint32_t K, uint64_t rowsC, uint32_t tm, uint32_t tn) {
+       uint32_t N, uint32_t K, uint64_t rowsC, uint32_t tm, uint32_t tn, uint32_t group) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *bars = (uint64_t *)(smem + STAGES * STAGE_BYTES);
@@ -144,7 +145,7 @@ k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         bool alive = true;
         for (uint32_t t = blockIdx.x; t < ntiles && alive; t += gridDim.x) {
             uint32_t mb, nb;
-            tile_coords(t, tm, tn, mb, nb);
+            tile_coords(t, tm, tn, group, mb, nb);
             for (uint32_t kb = 0; kb < nkb; kb++, it++) {
                 const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
                 if (!mbar_wait(smem_u32(&empty[s]), ph ^ 1)) { alive = false; break; }
@@ -201,7 +202,7 @@ k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         uint32_t tl = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, tl++) {
             uint32_t mb, nb;
-            tile_coords(t, tm, tn, mb, nb);
+            tile_coords(t, tm, tn, group, mb, nb);
             const uint32_t acc = tl & 1, aph = (tl >> 1) & 1;
             if (!mbar_wait(smem_u32(&tfull[acc]), aph)) break;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -294,7 +295,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, uint64_t C, uint64_t ldc,
-        uint32_t N, uint32_t K, uint64_t rowsC, uint32_t tm, uint32_t tn) {
+        uint32_t N, uint32_t K, uint64_t rowsC, uint32_t tm, uint32_t tn, uint32_t group) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *bars = (uint64_t *)(smem + STAGES2 * STAGE2_BYTES);
@@ -337,7 +338,7 @@ k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
         bool alive = true;
         for (uint32_t t = pair; t < ntiles && alive; t += npairs) {
             uint32_t mb, nb;
-            tile_coords(t, tm, tn, mb, nb);
+            tile_coords(t, tm, tn, group, mb, nb);
             const int row_a = (int)(mb * 2 * BM + rank * BM), row_b = (int)(nb * BN + rank * B_HALF);
             for (uint32_t kb = 0; kb < nkb; kb++, it++) {
                 const uint32_t s = it % STAGES2, ph = (it / STAGES2) & 1;
@@ -401,7 +402,7 @@ k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
         uint32_t tl = 0;
         for (uint32_t t = pair; t < ntiles; t += npairs, tl++) {
             uint32_t mb, nb;
-            tile_coords(t, tm, tn, mb, nb);
+            tile_coords(t, tm, tn, group, mb, nb);
             const uint32_t acc = tl & 1, aph = (tl >> 1) & 1;
             if (!mbar_wait(smem_u32(&tfull[acc]), aph)) break;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -545,6 +546,11 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
         const char *e = getenv("GD_GEMM_1SM");
         return e && e[0] == '1';
     }();
+    static const uint32_t group = [] {                 // raster group (m-blocks); tuning knob
+        const char *e = getenv("GD_GEMM_GROUP");
+        const int v = e ? atoi(e) : 0;
+        return (uint32_t)(v > 0 ? v : GROUP_M);
+    }();
     if (rC >= 2 * BM && !force1 && g.sms >= 2) {
         // 2-SM path: B staged in N halves per CTA
         CUtensorMap tmB2;
@@ -553,13 +559,13 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
         const uint32_t tm = (uint32_t)((rC + 2 * BM - 1) / (2 * BM)), tn = (N + BN - 1) / BN;
         const uint32_t ntiles = tm * tn, pairs_max = (uint32_t)g.sms / 2;
         const uint32_t grid = 2 * (ntiles < pairs_max ? ntiles : pairs_max);
-        k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, Cf, ldc, N, K, rC, tm, tn);
+        k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, Cf, ldc, N, K, rC, tm, tn, group);
         return cuda_status(cudaGetLastError());
     }
     const uint32_t tm = (uint32_t)((rC + BM - 1) / BM), tn = (N + BN - 1) / BN;   // rC <= M
     const uint32_t ntiles = tm * tn;
     const uint32_t grid = ntiles < (uint32_t)g.sms ? ntiles : (uint32_t)g.sms;
-    k_gemm<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, Cf, ldc, N, K, rC, tm, tn);
+    k_gemm<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, Cf, ldc, N, K, rC, tm, tn, group);
     return cuda_status(cudaGetLastError());
 }
 
