@@ -164,6 +164,9 @@ gd_status gd_check_range(const gd_arena *a, uint32_t id, uint64_t addr, uint64_t
  * gd_check_range.  Asynchronous on `stream` (host memory should be pinned).  */
 gd_status gd_memcpy_h2d(gd_arena *a, uint32_t id, uint64_t dst, const void *src, uint64_t n, void *stream);
 gd_status gd_memcpy_d2h(gd_arena *a, uint32_t id, void *dst, uint64_t src, uint64_t n, void *stream);
+/* Device-to-device transfer inside one partition ("within the GPU memory
+ * (e.g., cudaMemcpyD2D())"): both ranges are checked.         */
+gd_status gd_memcpy_d2d(gd_arena *a, uint32_t id, uint64_t dst, uint64_t src, uint64_t n, void *stream);
 
 /* Trusted fill of [base+offset, base+offset+nbytes) of a partition (K7):
  * pattern 0 = zeros (the scrub), 1 = the address-revealing word pattern

@@ -435,6 +435,19 @@ extern "C" gd_status gd_memcpy_d2h(gd_arena *a, uint32_t id, void *dst, uint64_t
     return e == cudaSuccess ? GD_OK : cuda_fail(e);
 }
 
+extern "C" gd_status gd_memcpy_d2d(gd_arena *a, uint32_t id, uint64_t dst, uint64_t src, uint64_t n, void *stream) {
+    if (!a) return GD_ERR_INVALID_ARG;
+    if (a->device < 0) return GD_ERR_UNSUPPORTED;
+    uint64_t b, s;
+    gd_status st = snapshot(a, id, &b, &s);
+    if (st != GD_OK) return st;
+    if (!range_ok(b, s, src, n) || !range_ok(b, s, dst, n)) return GD_ERR_OOB_RANGE;
+    if (n == 0) return GD_OK;
+    DeviceGuard dg(a->device);
+    cudaError_t e = cudaMemcpyAsync((void *)dst, (const void *)src, n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+    return e == cudaSuccess ? GD_OK : cuda_fail(e);
+}
+
 extern "C" gd_status gd_partition_fill(gd_arena *a, uint32_t id, uint32_t pattern, uint64_t offset,
                                        uint64_t nbytes, void *stream) {
     if (!a || pattern > 1) return GD_ERR_INVALID_ARG;

@@ -46,7 +46,10 @@ constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int THREADS = 256;
 constexpr uint32_t TMEM_COLS = ACC * BN;           // 512
-constexpr uint32_t GROUP_M = 16;                   // raster group (m-blocks)
+// raster group (m-blocks): probe (tools/gemm_group_probe.sh) at 8192^3 -- DRAM
+// reads 1.52 / 1.10 / 1.25 / 2.27 GB for groups 4 / 8 / 16 / 32, and under the
+// 1 kW power cap sustained TFLOP/s follow the DRAM traffic (8 is best)
+constexpr uint32_t GROUP_M = 8;
 
 // instruction descriptor: D f32, A/B bf16, both K-major, N=256, M=128
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);

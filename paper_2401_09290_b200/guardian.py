@@ -35,7 +35,7 @@ KIND_NAMES = ["copy", "saxpy", "gather", "scatter", "stencil", "gemm"]
 EXPORTED = [
     "gd_arena_create", "gd_arena_wrap", "gd_arena_destroy", "gd_arena_info",
     "gd_partition_alloc", "gd_partition_alloc_exact", "gd_partition_free", "gd_partition_get", "gd_malloc", "gd_free",
-    "gd_check_range", "gd_memcpy_h2d", "gd_memcpy_d2h", "gd_partition_fill",
+    "gd_check_range", "gd_memcpy_h2d", "gd_memcpy_d2h", "gd_memcpy_d2d", "gd_partition_fill",
     "gd_launch_fenced_copy", "gd_launch_fenced_saxpy", "gd_launch_fenced_gather",
     "gd_launch_fenced_scatter", "gd_launch_fenced_stencil", "gd_launch_fenced_gemm",
     "gd_schedule_round_robin", "gd_launcher_run",
@@ -91,6 +91,7 @@ def _load():
         "gd_check_range": [A, u32, u64, u64, P(i32)],
         "gd_memcpy_h2d": [A, u32, u64, vp, u64, vp],
         "gd_memcpy_d2h": [A, u32, vp, u64, u64, vp],
+        "gd_memcpy_d2d": [A, u32, u64, u64, u64, vp],
         "gd_partition_fill": [A, u32, u32, u64, u64, vp],
         "gd_launch_fenced_copy": [A, u32, i32, u64, u64, u64, vp],
         "gd_launch_fenced_saxpy": [A, u32, i32, f32, u64, u64, u64, vp],
@@ -265,6 +266,9 @@ class Arena:
 
     def memcpy_h2d(self, pid: int, dst: int, host_ptr: int, n: int, stream=None) -> None:
         _chk("gd_memcpy_h2d", _lib.gd_memcpy_h2d(self._h, pid, dst, host_ptr, n, _stream(stream)))
+
+    def memcpy_d2d(self, pid: int, dst: int, src: int, n: int, stream=None) -> None:
+        _chk("gd_memcpy_d2d", _lib.gd_memcpy_d2d(self._h, pid, dst, src, n, _stream(stream)))
 
     def memcpy_d2h(self, pid: int, host_ptr: int, src: int, n: int, stream=None) -> None:
         _chk("gd_memcpy_d2h", _lib.gd_memcpy_d2h(self._h, pid, host_ptr, src, n, _stream(stream)))

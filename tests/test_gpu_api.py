@@ -37,6 +37,13 @@ def test_checked_transfers(arenas):
     assert e.value.status == g.GD_ERR_OOB_RANGE
     assert np.array_equal(download(q.base, q.size), qbefore)
     a.memcpy_h2d(p.id, p.end - 16, host.data_ptr(), 16)          # ending exactly at end is fine
+    a.memcpy_d2d(p.id, p.base + 8192 * 16, p.base + 4096, 4096)
+    torch.cuda.synchronize()
+    assert np.array_equal(download(p.base + 8192 * 16, 4096), download(p.base + 4096, 4096))
+    for dst, src in ((q.base, p.base), (p.base, q.base), (p.end - 8, p.base)):
+        with pytest.raises(g.GuardianError) as e:
+            a.memcpy_d2d(p.id, dst, src, 64)
+        assert e.value.status == g.GD_ERR_OOB_RANGE
 
 
 def test_partitions_are_scrubbed_on_reuse(arenas):
