@@ -246,6 +246,19 @@ gd_status gd_schedule_round_robin(const gd_work *items, uint32_t n_items, uint32
 gd_status gd_launcher_run(gd_arena *a, const gd_work *items, uint32_t n_items, void *const *streams,
                           uint32_t n_streams, uint32_t *order_out);
 
+/* ---- captured steps (CUDA graphs) ------------------------------------------ */
+typedef struct gd_graph gd_graph;     /* opaque, library-owned */
+/* Capture one gd_launcher_run of `items` over n_streams library-owned tenant
+ * streams (fork / join through an origin stream) into a CUDA graph, every
+ * kernel with its partition descriptor baked in.  Items are validated first
+ * (nothing is captured if any is invalid).  Errors as gd_launcher_run.     */
+gd_status gd_graph_create(gd_arena *a, const gd_work *items, uint32_t n_items, uint32_t n_streams, gd_graph **out);
+/* Replay the captured step on `stream` with one host call.  Refuses with
+ * UNKNOWN_PARTITION (nothing launched) if any partition the graph fences was
+ * freed or re-allocated since capture: stale bounds are never used.        */
+gd_status gd_graph_launch(gd_graph *g, void *stream);
+gd_status gd_graph_destroy(gd_graph *g);
+
 /* ---- statistics --------------------------------- */
 /* Synchronises the device, then returns tenant id's counters, or the sum over
  * all tenants for GD_ALL_TENANTS.                                            */

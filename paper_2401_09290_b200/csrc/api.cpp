@@ -317,6 +317,7 @@ gd_status carve(gd_arena *a, uint64_t size, bool pow2, gd_partition_info *out) {
     p.size = size;
     p.order = order;
     p.pow2 = pow2;
+    p.gen = a->next_gen++;
     p.sub.init(size);
     for (unsigned k = 0; k < GD_NUM_KINDS; k++) a->host[id][k] = HostCounters{};
     fill_info(id, p, out);
@@ -473,7 +474,8 @@ namespace gd {
 
 // Validate `w` (dry) or validate and launch it.  Structural errors are
 // returned before anything is issued.
-gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry) {
+gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry, bool account, uint64_t *bytes_out,
+                   uint64_t *flops_out) {
     if (!a) return GD_ERR_INVALID_ARG;
     if (w.mode > GD_MODE_MODULO || w.kind >= GD_NUM_KINDS) return GD_ERR_INVALID_ARG;
     uint64_t base, size;
@@ -565,7 +567,9 @@ gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry)
         }
     }
     if (e != cudaSuccess) return cuda_fail(e);
-    {
+    if (bytes_out) *bytes_out = bytes;
+    if (flops_out) *flops_out = flops;
+    if (account) {
         std::lock_guard<std::mutex> lk(a->mu);
         HostCounters &hc = a->host[w.tenant][w.kind];
         hc.launches++;
@@ -576,6 +580,15 @@ gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry)
 }
 
 gd_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GD_OK : cuda_fail(e); }
+
+gd_status partition_snapshot(gd_arena *a, uint32_t id, uint64_t *base, uint64_t *size, uint64_t *gen) {
+    std::lock_guard<std::mutex> lk(a->mu);
+    if (id >= GD_MAX_TENANTS || !a->parts[id].live) return GD_ERR_UNKNOWN_PARTITION;
+    *base = a->parts[id].base;
+    *size = a->parts[id].size;
+    *gen = a->parts[id].gen;
+    return GD_OK;
+}
 
 }  // namespace gd
 

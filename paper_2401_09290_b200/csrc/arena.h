@@ -52,6 +52,7 @@ struct Partition {
     uint64_t base = 0, size = 0;
     unsigned order = 0;
     bool pow2 = true;              // false: exact-size partition (modulo / check / none modes)
+    uint64_t gen = 0;              // allocation generation (captured graphs check it)
     SubAlloc sub;
 };
 
@@ -80,5 +81,6 @@ struct gd_arena {
     void *zero_buf = nullptr;        // trusted zero row for operands with no rows (gemm.cu)
     uint64_t zero_bytes = 0;
     int sms = 148;
+    uint64_t next_gen = 1;
     std::mutex mu;
 };

@@ -95,6 +95,69 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
+// ---------------------------------------------------------------------------
+// Epilogue: one 32-row x 32-column chunk of the accumulator (the warp's TMEM
+// lanes) -> bf16 -> shared-memory staging -> TMA store through the C tensor
+// map.  The map's extent is the descriptor-fenced row count of C, so rows at
+// or past it (and columns >= N) are dropped by the TMA unit itself: the C
+// fence lives in the tensor map exactly like A's and B's.
+// ---------------------------------------------------------------------------
+constexpr uint32_t EPI_CHUNK_BYTES = 32 * 32 * 2;              // 2 KB
+constexpr uint32_t EPI_BYTES = 4 * 2 * EPI_CHUNK_BYTES;        // 4 warps x double buffer
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// chunk index c of this warp's tile: waits (lane 0) for the store that last
+// used the staging buffer, writes the bf16 rows, issues the TMA store.
+__device__ __forceinline__ void epi_store_chunk(const CUtensorMap *tmC, uint32_t stage_base, uint32_t chunk_no,
+                                                const uint32_t (&v)[32], uint32_t lane, int col0, int row0) {
+    const uint32_t buf = stage_base + (chunk_no & 1) * EPI_CHUNK_BYTES;
+    if (chunk_no >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+    uint32_t p[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+        p[e] = *reinterpret_cast<uint32_t *>(&h);
+    }
+    // row `lane` is 64 bytes: four 16-byte pieces, written in a lane-rotated
+    // order so a warp's 16-byte stores spread over all banks (4 wavefronts)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const uint32_t qq = (q + (lane >> 1)) & 3;
+        const uint32_t a0 = qq == 0 ? p[0] : qq == 1 ? p[4] : qq == 2 ? p[8] : p[12];
+        const uint32_t a1 = qq == 0 ? p[1] : qq == 1 ? p[5] : qq == 2 ? p[9] : p[13];
+        const uint32_t a2 = qq == 0 ? p[2] : qq == 1 ? p[6] : qq == 2 ? p[10] : p[14];
+        const uint32_t a3 = qq == 0 ? p[3] : qq == 1 ? p[7] : qq == 2 ? p[11] : p[15];
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 64 + qq * 16), "r"(a0), "r"(a1),
+                     "r"(a2), "r"(a3)
+                     : "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmC),
+                     "r"(buf), "r"(col0), "r"(row0)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+}
+
+__device__ __forceinline__ void epi_drain(uint32_t lane) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+}
+
 // grouped raster: tiles t = 0..tm*tn-1 -> (m_blk, n_blk)
 __device__ __forceinline__ void tile_coords(uint32_t t, uint32_t tm, uint32_t tn, uint32_t group, uint32_t &mb,
                                             uint32_t &nb) {
@@ -279,7 +342,7 @@ constexpr uint32_t IDESC2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN 
 constexpr uint32_t B_HALF = BN / 2;                           // B rows staged per CTA
 constexpr uint32_t STAGE2_BYTES = A_BYTES + B_HALF * BK * 2;  // 32 KB
 constexpr int STAGES2 = 6;
-constexpr uint32_t SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 1024 + 256;
+constexpr uint32_t SMEM2_BYTES = STAGES2 * STAGE2_BYTES + EPI_BYTES + 1024 + 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -297,11 +360,12 @@ __device__ __forceinline__ void cluster_sync_all() {
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, uint64_t C, uint64_t ldc,
-        uint32_t N, uint32_t K, uint64_t rowsC, uint32_t tm, uint32_t tn, uint32_t group) {
+k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+        const __grid_constant__ CUtensorMap tmC, uint32_t K, uint32_t tm, uint32_t tn, uint32_t group) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t *bars = (uint64_t *)(smem + STAGES2 * STAGE2_BYTES);
+    uint8_t *epi = smem + STAGES2 * STAGE2_BYTES;                  // C staging, 16 KB
+    uint64_t *bars = (uint64_t *)(epi + EPI_BYTES);
     uint64_t *full = bars, *empty = bars + STAGES2;
     uint64_t *tfull = bars + 2 * STAGES2, *tempty = bars + 2 * STAGES2 + ACC;
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * STAGES2 + 2 * ACC);
@@ -402,30 +466,20 @@ k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
     } else if (warp >= 4) {
         // ---------------- epilogue (both CTAs: own 128 rows) ----------------
         const uint32_t wq = warp - 4;
-        uint32_t tl = 0;
+        const uint32_t stage_base = smem_u32(epi) + wq * 2 * EPI_CHUNK_BYTES;
+        uint32_t tl = 0, chunk_no = 0;
         for (uint32_t t = pair; t < ntiles; t += npairs, tl++) {
             uint32_t mb, nb;
             tile_coords(t, tm, tn, group, mb, nb);
             const uint32_t acc = tl & 1, aph = (tl >> 1) & 1;
             if (!mbar_wait(smem_u32(&tfull[acc]), aph)) break;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t row = (uint64_t)mb * 2 * BM + rank * BM + wq * 32 + lane;
-            const bool store_row = row < rowsC;
-            const uint32_t n0 = nb * BN;
+            const int row0 = (int)(mb * 2 * BM + rank * BM + wq * 32);
+            const int n0 = (int)(nb * BN);
 #pragma unroll 1
             for (int c = 0; c < BN / 32; c++) {
                 uint32_t v[32];
-                const uint32_t taddr = tmem + ((wq * 32u) << 16) + acc * BN + (uint32_t)(c * 32);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                tmem_ld32(tmem + ((wq * 32u) << 16) + acc * BN + (uint32_t)(c * 32), v);
                 if (c == BN / 32 - 1) {
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     __syncwarp();
@@ -435,25 +489,10 @@ k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
                                      : "memory");
                     }
                 }
-                if (store_row) {
-#pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        const uint32_t col = n0 + c * 32 + q * 8;
-                        if (col < N) {
-                            uint32_t p[4];
-#pragma unroll
-                            for (int e = 0; e < 4; e++) {
-                                __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * e]),
-                                                                         __uint_as_float(v[q * 8 + 2 * e + 1]));
-                                p[e] = *reinterpret_cast<uint32_t *>(&h);
-                            }
-                            uint4 *dst = reinterpret_cast<uint4 *>(C + 2 * (row * ldc + col));
-                            *dst = make_uint4(p[0], p[1], p[2], p[3]);
-                        }
-                    }
-                }
+                epi_store_chunk(&tmC, stage_base, chunk_no++, v, lane, n0 + c * 32, row0);
             }
         }
+        epi_drain(lane);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -475,6 +514,19 @@ bool make_map(CUtensorMap *m, uint64_t addr, uint64_t K, uint64_t rows, uint64_t
     CUresult r = drv().TensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void *)addr, dims, strides, box,
                                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// C's store map: N columns x rowsC rows (the descriptor-fenced extent), boxes
+// of 32 x 32 bf16, no swizzle (the staging tile is plain row-major).
+bool make_map_c(CUtensorMap *m, uint64_t addr, uint64_t N, uint64_t rows, uint64_t ld) {
+    const cuuint64_t dims[2] = {N, rows};
+    const cuuint64_t strides[1] = {ld * 2};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = drv().TensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void *)addr, dims, strides, box,
+                                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -501,6 +553,37 @@ uint64_t desc_rows(int mode, uint64_t base, uint64_t size, uint64_t p, uint64_t 
     return valid < rows ? valid : rows;
 }
 
+// Trusted all-zero row of >= 2K bytes outside every partition (allocating
+// synchronises, so graph capture calls gemm_prepare first).
+gd_status ensure_zero_row(gd_arena *a, uint64_t K) {
+    std::lock_guard<std::mutex> lk(a->mu);
+    if (a->zero_bytes >= 2ull * K) return GD_OK;
+    if (a->zero_buf) cudaFree(a->zero_buf);
+    a->zero_buf = nullptr;
+    a->zero_bytes = 0;
+    cudaError_t e = cudaMalloc(&a->zero_buf, 2ull * K);
+    if (e == cudaSuccess) e = cudaMemset(a->zero_buf, 0, 2ull * K);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_status(e);
+    a->zero_bytes = 2ull * K;
+    return GD_OK;
+}
+
+// Everything gemm_dispatch might need to do outside a stream (one-time
+// function attributes, the zero row), so that it can run under capture.
+gd_status gemm_prepare(gd_arena *a, const gd_work &w, uint64_t base, uint64_t size) {
+    static bool attr = [] {
+        return cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) == cudaSuccess &&
+               cudaFuncSetAttribute(k_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES) == cudaSuccess;
+    }();
+    if (!attr) return cuda_status(cudaErrorInvalidValue);
+    const uint32_t M = w.u32[0], N = w.u32[1], K = w.u32[2];
+    uint64_t f;
+    const uint64_t rA = desc_rows(w.mode, base, size, w.ptr[1], M, 2ull * K, 2ull * w.u64[0], &f);
+    const uint64_t rB = desc_rows(w.mode, base, size, w.ptr[2], N, 2ull * K, 2ull * w.u64[1], &f);
+    return (rA == 0 || rB == 0) ? ensure_zero_row(a, K) : GD_OK;
+}
+
 gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t size, cudaStream_t s,
                         const Geom &g) {
     const uint32_t M = w.u32[0], N = w.u32[1], K = w.u32[2];
@@ -522,17 +605,8 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
     if (rA == 0 || rB == 0) {
         // an operand with no rows reads as zeros: point its map at a trusted
         // zero row outside every partition
-        std::lock_guard<std::mutex> lk(a->mu);
-        if (a->zero_bytes < 2ull * K) {
-            if (a->zero_buf) cudaFree(a->zero_buf);
-            a->zero_buf = nullptr;
-            a->zero_bytes = 0;
-            cudaError_t e = cudaMalloc(&a->zero_buf, 2ull * K);
-            if (e == cudaSuccess) e = cudaMemset(a->zero_buf, 0, 2ull * K);
-            if (e == cudaSuccess) e = cudaDeviceSynchronize();
-            if (e != cudaSuccess) return cuda_status(e);
-            a->zero_bytes = 2ull * K;
-        }
+        gd_status zs = ensure_zero_row(a, K);
+        if (zs != GD_OK) return zs;
         if (rA == 0) { Af = (uint64_t)a->zero_buf; rA = 1; ldA = K; }
         if (rB == 0) { Bf = (uint64_t)a->zero_buf; rB = 1; ldB = K; }
     }
@@ -556,13 +630,14 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
     }();
     if (rC >= 2 * BM && !force1 && g.sms >= 2) {
         // 2-SM path: B staged in N halves per CTA
-        CUtensorMap tmB2;
+        CUtensorMap tmB2, tmC;
         std::memset(&tmB2, 0, sizeof(tmB2));
-        if (!make_map(&tmB2, Bf, K, rB, ldB, B_HALF)) return GD_ERR_UNSUPPORTED;
+        std::memset(&tmC, 0, sizeof(tmC));
+        if (!make_map(&tmB2, Bf, K, rB, ldB, B_HALF) || !make_map_c(&tmC, Cf, N, rC, ldc)) return GD_ERR_UNSUPPORTED;
         const uint32_t tm = (uint32_t)((rC + 2 * BM - 1) / (2 * BM)), tn = (N + BN - 1) / BN;
         const uint32_t ntiles = tm * tn, pairs_max = (uint32_t)g.sms / 2;
         const uint32_t grid = 2 * (ntiles < pairs_max ? ntiles : pairs_max);
-        k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, Cf, ldc, N, K, rC, tm, tn, group);
+        k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, tmC, K, tm, tn, group);
         return cuda_status(cudaGetLastError());
     }
     const uint32_t tm = (uint32_t)((rC + BM - 1) / BM), tn = (N + BN - 1) / BN;   // rC <= M

@@ -40,7 +40,7 @@ EXPORTED = [
     "gd_launch_fenced_scatter", "gd_launch_fenced_stencil", "gd_launch_fenced_gemm",
     "gd_schedule_round_robin", "gd_launcher_run",
     "gd_stats", "gd_stats_reset", "gd_stats_device_ptr", "gd_status_str", "gd_last_cuda_error", "gd_version",
-    "gd_device_flags",
+    "gd_device_flags", "gd_graph_create", "gd_graph_launch", "gd_graph_destroy",
 ]
 
 
@@ -105,6 +105,9 @@ def _load():
         "gd_stats_reset": [A, u32],
         "gd_stats_device_ptr": [A, P(u64)],
         "gd_device_flags": [A, P(u32)],
+        "gd_graph_create": [A, P(gd_work), u32, u32, P(vp)],
+        "gd_graph_launch": [vp, vp],
+        "gd_graph_destroy": [vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -187,6 +190,27 @@ class Partition:
 
     def __repr__(self):
         return f"Partition(id={self.id}, base={self.base:#x}, size={self.size:#x})"
+
+
+class Graph:
+    """A captured multi-tenant step (gd_graph)."""
+
+    def __init__(self, h):
+        self._h = h
+
+    def launch(self, stream=None) -> None:
+        _chk("gd_graph_launch", _lib.gd_graph_launch(self._h, _stream(stream)))
+
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            _chk("gd_graph_destroy", _lib.gd_graph_destroy(self._h))
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Arena:
@@ -303,6 +327,13 @@ class Arena:
         _chk("gd_launch_fenced_gemm",
              _lib.gd_launch_fenced_gemm(self._h, pid, _mode(mode), C, A, B, M, N, K, lda, ldb, ldc,
                                         _stream(stream)))
+
+    def graph(self, items, n_streams: int) -> "Graph":
+        """Capture one launcher step of `items` into a CUDA graph."""
+        arr = (gd_work * len(items))(*items)
+        h = ctypes.c_void_p()
+        _chk("gd_graph_create", _lib.gd_graph_create(self._h, arr, len(items), n_streams, ctypes.byref(h)))
+        return Graph(h)
 
     def launcher_run(self, items, streams):
         arr = (gd_work * len(items))(*items)

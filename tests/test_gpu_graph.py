@@ -1,0 +1,96 @@
+"""Captured multi-tenant steps (gd_graph_*): a replay computes exactly what
+the launcher computes (bit-exact against the oracle for the C1 toy, in mask
+and check mode, violations included), accounting counts every replay, a
+graph refuses to replay after any partition it fences was re-allocated, and
+for launch-bound steps the replay is cheaper than issuing kernel by kernel."""
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2401_09290_b200 import guardian as g
+from tests.gpu_util import download, first_diff, upload
+
+pytestmark = pytest.mark.gpu
+
+
+def _toy(arenas):
+    a = arenas(synth.C1_ARENA)
+    parts = [a.partition_alloc(synth.C1_PART) for _ in range(synth.C1_TENANTS)]
+    toy = synth.toy_gather()
+    host = np.zeros(a.size, np.uint8)
+    for t, p in enumerate(parts):
+        o = p.base - a.base
+        host[o:o + 4 * synth.C1_TABLE_N] = toy.tables[t].view(np.uint8)
+        host[o + synth.C1_IDX_OFF:o + synth.C1_IDX_OFF + 4 * synth.C1_N] = toy.idx[t].view(np.uint8)
+    upload(a.base, host)
+    return a, parts, toy, host
+
+
+@pytest.mark.parametrize("mode", ["mask", "check"])
+def test_graph_replay_matches_oracle(arenas, mode):
+    a, parts, toy, host = _toy(arenas)
+    items = [g.work(p.id, g.GD_KIND_GATHER, mode, ptr=(p.base + synth.C1_OUT_OFF, p.base, p.base + synth.C1_IDX_OFF),
+                    u64=(synth.C1_N,), u32=(1,)) for p in parts]
+    graph = a.graph(items, n_streams=4)
+    a.stats_reset()
+    for _ in range(3):
+        graph.launch()
+    torch.cuda.synchronize()
+    mem = oracle.Mem(a.base, buf=host.copy())
+    for p in parts:
+        oracle.gather(mem, p.base, p.size, mode, p.base + synth.C1_OUT_OFF, p.base, p.base + synth.C1_IDX_OFF,
+                      synth.C1_N)
+    got = download(a.base, a.size)
+    assert np.array_equal(got, mem.buf), first_diff(got, mem.buf)
+    st = a.stats()
+    assert st["launches"] == 3 * len(items)
+    assert st["violations"] == (3 * toy.n_planted if mode == "check" else 0)
+    graph.close()
+
+
+def test_graph_refuses_stale_partitions(arenas):
+    a, parts, _, _ = _toy(arenas)
+    items = [g.work(parts[1].id, g.GD_KIND_COPY, "mask", ptr=(parts[1].base + 4096, parts[1].base), u64=(4096,))]
+    graph = a.graph(items, n_streams=1)
+    graph.launch()
+    a.partition_free(parts[1].id)
+    with pytest.raises(g.GuardianError) as e:
+        graph.launch()
+    assert e.value.status == g.GD_ERR_UNKNOWN_PARTITION
+    q = a.partition_alloc(synth.C1_PART)             # same id and base, new generation
+    assert q.id == parts[1].id and q.base == parts[1].base
+    with pytest.raises(g.GuardianError):
+        graph.launch()
+    graph.close()
+
+
+def test_graph_is_cheaper_for_small_steps(arenas):
+    """64 tiny fenced kernels across 8 tenants: one graph replay vs 64 calls."""
+    a = arenas(8 << 20)
+    parts = [a.partition_alloc(1 << 20) for _ in range(8)]
+    items = [g.work(p.id, g.GD_KIND_COPY, "mask", ptr=(p.base + 4096 * (k + 1), p.base), u64=(4096,))
+             for k in range(8) for p in parts]
+    streams = [torch.cuda.Stream() for _ in parts]
+    graph = a.graph(items, n_streams=8)
+    for _ in range(5):
+        a.launcher_run(items, streams)
+        graph.launch()
+    torch.cuda.synchronize()
+    reps = 50
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        a.launcher_run(items, streams)
+    torch.cuda.synchronize()
+    t_launcher = (time.perf_counter() - t0) / reps
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        graph.launch()
+    torch.cuda.synchronize()
+    t_graph = (time.perf_counter() - t0) / reps
+    print(f"64-kernel step: launcher {t_launcher * 1e6:.1f} us, graph {t_graph * 1e6:.1f} us")
+    assert t_graph < t_launcher
+    graph.close()
