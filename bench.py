@@ -265,6 +265,50 @@ class Workload:
         torch.cuda.synchronize(self.device)
         return start.elapsed_time(stop), nbytes * launches, flops * launches, planted * launches
 
+    def kernel_table(self, reps=5):
+        """Solo launches of every kernel at its BASELINE size in every mode,
+        interleaved, CUDA events on one stream (after c5(): tenant 3/4 hold
+        the C3 gather / scatter layout with 1 % OOB, tenant 6 the GEMM).
+        Returns {kernel: {mode: {"ms", "work", "unit"}}} (per GPU, medians)."""
+        torch, parts = self.torch, self.parts
+        n_idx, n = 1 << 26, 8192
+        H = W = 32768
+        p0, p3, p4, p5, p6 = parts[0], parts[3], parts[4], parts[5], parts[6]
+        a = self.arena
+        kern = {
+            "copy_4GiB": (lambda m, s: a.copy(p0.id, m, p0.base + OFF_DST, p0.base + OFF_SRC, COPY_BYTES, stream=s),
+                          BYTES_COPY, "GB/s"),
+            "saxpy_2^30": (lambda m, s: a.saxpy(p0.id, m, ALPHA, p0.base + OFF_X, p0.base + OFF_Y, SAXPY_N, stream=s),
+                           BYTES_SAXPY, "GB/s"),
+            "gather_2^26_1pct_oob": (lambda m, s: a.gather(p3.id, m, p3.base + 2 * GiB + GiB // 4, p3.base,
+                                                           p3.base + 2 * GiB, n_idx, stream=s), 12 * n_idx, "GB/s"),
+            "scatter_2^26_1pct_oob": (lambda m, s: a.scatter(p4.id, m, p4.base, p4.base + 2 * GiB,
+                                                             p4.base + 2 * GiB + GiB // 4, n_idx, stream=s),
+                                      16 * n_idx, "GB/s"),
+            "stencil_32768^2": (lambda m, s: a.stencil(p5.id, m, p5.base + 8 * GiB, p5.base + 4 * GiB, H, W, W,
+                                                       0.5, 0.125, stream=s), 8 * (H - 2) * (W - 2), "GB/s"),
+            "gemm_8192^3": (lambda m, s: a.gemm(p6.id, m, p6.base + 2 * n * n * 2, p6.base, p6.base + n * n * 2,
+                                                n, n, n, n, n, n, stream=s), 2 * n ** 3, "TFLOP/s"),
+        }
+        s = self.streams[0]
+        out = {}
+        modes = ("none", "mask", "check", "modulo")
+        for name, (fn, work, unit) in kern.items():
+            times = {m: [] for m in modes}
+            with torch.cuda.stream(s):
+                for m in modes:
+                    fn(m, s)
+                for _ in range(reps):
+                    for m in modes:
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(s)
+                        fn(m, s)
+                        e1.record(s)
+                        e1.synchronize()
+                        times[m].append(e0.elapsed_time(e1))
+            out[name] = {m: {"ms": statistics.median(v), "work": work, "unit": unit} for m, v in times.items()}
+        return out
+
     def e2e(self, mode, steps, warmup):
         """Through the public API with HOST buffers: every step copies each
         tenant's inputs host->device (checked transfers, gd_memcpy_h2d), runs
@@ -389,6 +433,18 @@ def run_gpu(args):
         c5["violations_expected"] = c5_expected                       # 3 x 671,089 x launches x G
         c5["violations_exact"] = int(red[0]) == c5_expected
 
+    # ---- every kernel x every mode at the BASELINE sizes ----
+    table = None
+    if not args.no_c5:
+        table = w.kernel_table(reps=args.table_reps)
+        for k, row in table.items():                                   # max time over ranks
+            for m in list(row):
+                t = allreduce([row[m]["ms"]])[0]
+                row[m] = {"ms": round(t, 4), row[m]["unit"]: round(world * row[m]["work"] / (t / 1e3) /
+                                                                    (1e9 if row[m]["unit"] == "GB/s" else 1e12), 1)}
+            for m in ("mask", "check", "modulo"):
+                row[m]["overhead_pct"] = round(100 * (row[m]["ms"] / row["none"]["ms"] - 1), 2)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(seconds=args.cpu_seconds)
@@ -410,6 +466,7 @@ def run_gpu(args):
             "clocks": clk.summary(),
             "stats_allreduced": {"violations": int(red[0]), "launches": int(red[1]), "bytes": int(red[2])},
             "multi_tenant_c5": c5,
+            "kernels_all_modes": table,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -525,6 +582,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the mixed multi-tenant (configs[4]) measurement")
     ap.add_argument("--c5-launches", type=int, default=20)
+    ap.add_argument("--table-reps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

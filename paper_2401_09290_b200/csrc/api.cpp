@@ -135,6 +135,11 @@ gd_status snapshot(gd_arena *a, uint32_t id, uint64_t *base, uint64_t *size) {
 
 bool mul_ok(uint64_t a, uint64_t b, uint64_t *r) { return !__builtin_mul_overflow(a, b, r); }
 
+bool tenant_live(gd_arena *a, uint32_t id) {
+    std::lock_guard<std::mutex> lk(a->mu);
+    return id < GD_MAX_TENANTS && a->parts[id].live;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -680,7 +685,7 @@ extern "C" gd_status gd_launch_fenced_gemm(gd_arena *a, uint32_t id, gd_mode mod
 extern "C" gd_status gd_stats(gd_arena *a, uint32_t id, gd_stats_t *out) {
     if (!a || !out) return GD_ERR_INVALID_ARG;
     std::memset(out, 0, sizeof(*out));
-    if (id != GD_ALL_TENANTS && (id >= GD_MAX_TENANTS || !a->parts[id].live)) return GD_ERR_UNKNOWN_PARTITION;
+    if (id != GD_ALL_TENANTS && !tenant_live(a, id)) return GD_ERR_UNKNOWN_PARTITION;
     unsigned long long dev[GD_MAX_TENANTS * GD_NUM_KINDS];
     std::memset(dev, 0, sizeof(dev));
     if (a->device >= 0) {
@@ -707,7 +712,7 @@ extern "C" gd_status gd_stats(gd_arena *a, uint32_t id, gd_stats_t *out) {
 
 extern "C" gd_status gd_stats_reset(gd_arena *a, uint32_t id) {
     if (!a) return GD_ERR_INVALID_ARG;
-    if (id != GD_ALL_TENANTS && (id >= GD_MAX_TENANTS || !a->parts[id].live)) return GD_ERR_UNKNOWN_PARTITION;
+    if (id != GD_ALL_TENANTS && !tenant_live(a, id)) return GD_ERR_UNKNOWN_PARTITION;
     if (a->device >= 0) {
         DeviceGuard dg(a->device);
         cudaError_t e = cudaDeviceSynchronize();

@@ -24,8 +24,10 @@
 //              (2 x 256 columns) so the epilogue of tile i overlaps the
 //              mainloop of tile i+1;
 //   warp 2     TMEM allocator (512 columns);
-//   warps 4-7  epilogue: tcgen05.ld 32x32b -> bf16 -> st.global, rows
-//              clamped to the C extent, then release the accumulator.
+//   warps 4-7  epilogue: tcgen05.ld 32x32b -> bf16 -> shared-memory staging
+//              -> TMA store through C's tensor map, whose extent is the
+//              descriptor-fenced row count (TMA drops rows past it), then
+//              release the accumulator.
 // All waits are bounded: a kernel that cannot make progress sets a device
 // error word and exits instead of hanging the shared context.
 #include <cuda.h>
@@ -43,7 +45,9 @@ constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4, ACC = 2;
 constexpr uint32_t A_BYTES = BM * BK * 2;          // 16 KB
 constexpr uint32_t B_BYTES = BN * BK * 2;          // 32 KB
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t EPI_CHUNK_BYTES = 32 * 32 * 2;              // C staging chunk: 32 x 32 bf16
+constexpr uint32_t EPI_BYTES = 4 * 2 * EPI_CHUNK_BYTES;        // 4 epilogue warps x double buffer
+constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int THREADS = 256;
 constexpr uint32_t TMEM_COLS = ACC * BN;           // 512
 // raster group (m-blocks): probe (tools/gemm_group_probe.sh) at 8192^3 -- DRAM
@@ -102,9 +106,6 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // or past it (and columns >= N) are dropped by the TMA unit itself: the C
 // fence lives in the tensor map exactly like A's and B's.
 // ---------------------------------------------------------------------------
-constexpr uint32_t EPI_CHUNK_BYTES = 32 * 32 * 2;              // 2 KB
-constexpr uint32_t EPI_BYTES = 4 * 2 * EPI_CHUNK_BYTES;        // 4 warps x double buffer
-
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -170,11 +171,12 @@ __device__ __forceinline__ void tile_coords(uint32_t t, uint32_t tm, uint32_t tn
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
-k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, uint64_t C, uint64_t ldc,
-       uint32_t N, uint32_t K, uint64_t rowsC, uint32_t tm, uint32_t tn, uint32_t group) {
+k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+       const __grid_constant__ CUtensorMap tmC, uint32_t K, uint32_t tm, uint32_t tn, uint32_t group) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t *bars = (uint64_t *)(smem + STAGES * STAGE_BYTES);
+    uint8_t *epi = smem + STAGES * STAGE_BYTES;                    // C staging, 16 KB
+    uint64_t *bars = (uint64_t *)(epi + EPI_BYTES);
     uint64_t *full = bars, *empty = bars + STAGES;
     uint64_t *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + ACC;
     uint32_t *tmem_slot = (uint32_t *)(bars + 2 * STAGES + 2 * ACC);
@@ -263,32 +265,21 @@ k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                          : "memory");
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue: TMEM -> registers -> bf16 -> global ----------------
+        // ---------------- epilogue: TMEM -> registers -> bf16 -> smem -> TMA store ----------------
         const uint32_t wq = warp - 4;                  // TMEM lanes 32*wq .. 32*wq+31
-        uint32_t tl = 0;
+        const uint32_t stage_base = smem_u32(epi) + wq * 2 * EPI_CHUNK_BYTES;
+        uint32_t tl = 0, chunk_no = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, tl++) {
             uint32_t mb, nb;
             tile_coords(t, tm, tn, group, mb, nb);
             const uint32_t acc = tl & 1, aph = (tl >> 1) & 1;
             if (!mbar_wait(smem_u32(&tfull[acc]), aph)) break;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t row = (uint64_t)mb * BM + wq * 32 + lane;
-            const bool store_row = row < rowsC;
-            const uint32_t n0 = nb * BN;
+            const int row0 = (int)(mb * BM + wq * 32), n0 = (int)(nb * BN);
 #pragma unroll 1
             for (int c = 0; c < BN / 32; c++) {
                 uint32_t v[32];
-                const uint32_t taddr = tmem + ((wq * 32u) << 16) + acc * BN + (uint32_t)(c * 32);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                tmem_ld32(tmem + ((wq * 32u) << 16) + acc * BN + (uint32_t)(c * 32), v);
                 if (c == BN / 32 - 1) {
                     // accumulator fully read: hand it back to the MMA warp
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -297,25 +288,10 @@ k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc]))
                                      : "memory");
                 }
-                if (store_row) {
-#pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        const uint32_t col = n0 + c * 32 + q * 8;
-                        if (col < N) {
-                            uint32_t p[4];
-#pragma unroll
-                            for (int e = 0; e < 4; e++) {
-                                __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * e]),
-                                                                         __uint_as_float(v[q * 8 + 2 * e + 1]));
-                                p[e] = *reinterpret_cast<uint32_t *>(&h);
-                            }
-                            uint4 *dst = reinterpret_cast<uint4 *>(C + 2 * (row * ldc + col));
-                            *dst = make_uint4(p[0], p[1], p[2], p[3]);
-                        }
-                    }
-                }
+                epi_store_chunk(&tmC, stage_base, chunk_no++, v, lane, n0 + c * 32, row0);
             }
         }
+        epi_drain(lane);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -610,10 +586,11 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
         if (rA == 0) { Af = (uint64_t)a->zero_buf; rA = 1; ldA = K; }
         if (rB == 0) { Bf = (uint64_t)a->zero_buf; rB = 1; ldB = K; }
     }
-    CUtensorMap tmA, tmB;
+    CUtensorMap tmA, tmB, tmC;
     std::memset(&tmA, 0, sizeof(tmA));
     std::memset(&tmB, 0, sizeof(tmB));
-    if (!make_map(&tmA, Af, K, rA, ldA, BM) || !make_map(&tmB, Bf, K, rB, ldB, BN)) return GD_ERR_UNSUPPORTED;
+    std::memset(&tmC, 0, sizeof(tmC));
+    if (!make_map(&tmA, Af, K, rA, ldA, BM) || !make_map_c(&tmC, Cf, N, rC, ldc)) return GD_ERR_UNSUPPORTED;
     static bool attr = [] {
         return cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) == cudaSuccess &&
                cudaFuncSetAttribute(k_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES) == cudaSuccess;
@@ -630,20 +607,20 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
     }();
     if (rC >= 2 * BM && !force1 && g.sms >= 2) {
         // 2-SM path: B staged in N halves per CTA
-        CUtensorMap tmB2, tmC;
+        CUtensorMap tmB2;
         std::memset(&tmB2, 0, sizeof(tmB2));
-        std::memset(&tmC, 0, sizeof(tmC));
-        if (!make_map(&tmB2, Bf, K, rB, ldB, B_HALF) || !make_map_c(&tmC, Cf, N, rC, ldc)) return GD_ERR_UNSUPPORTED;
+        if (!make_map(&tmB2, Bf, K, rB, ldB, B_HALF)) return GD_ERR_UNSUPPORTED;
         const uint32_t tm = (uint32_t)((rC + 2 * BM - 1) / (2 * BM)), tn = (N + BN - 1) / BN;
         const uint32_t ntiles = tm * tn, pairs_max = (uint32_t)g.sms / 2;
         const uint32_t grid = 2 * (ntiles < pairs_max ? ntiles : pairs_max);
         k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, tmC, K, tm, tn, group);
         return cuda_status(cudaGetLastError());
     }
+    if (!make_map(&tmB, Bf, K, rB, ldB, BN)) return GD_ERR_UNSUPPORTED;
     const uint32_t tm = (uint32_t)((rC + BM - 1) / BM), tn = (N + BN - 1) / BN;   // rC <= M
     const uint32_t ntiles = tm * tn;
     const uint32_t grid = ntiles < (uint32_t)g.sms ? ntiles : (uint32_t)g.sms;
-    k_gemm<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, Cf, ldc, N, K, rC, tm, tn, group);
+    k_gemm<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, tmC, K, tm, tn, group);
     return cuda_status(cudaGetLastError());
 }
 
