@@ -548,6 +548,14 @@ gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry,
     fd.size = size;
     fd.inv = recip64(size);
     fd.viol = a->d_stats + (uint64_t)w.tenant * GD_NUM_KINDS + w.kind;
+    // GD_CHECK_PER_ACCESS=1: no tile-level range test (measures the paper's
+    // per-access check cost; results are identical either way)
+    static const uint32_t no_hoist = [] {
+        const char *e = getenv("GD_CHECK_PER_ACCESS");
+        return (e && e[0] == '1') ? kNoHoist : 0u;
+    }();
+    fd.flags = no_hoist;
+    fd.pad_ = 0;
     const Geom g{a->sms};
     DeviceGuard dg(a->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err);

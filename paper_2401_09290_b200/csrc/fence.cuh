@@ -62,7 +62,7 @@ struct Fence {
 // touch or cross the partition edge pay for per-access checks.
 __device__ __forceinline__ bool range_in(const FenceDesc &fd, uint64_t a, uint64_t len) {
     const uint64_t off = a - fd.base;
-    return len <= fd.size && off <= fd.size - len;
+    return !(fd.flags & kNoHoist) && len <= fd.size && off <= fd.size - len;
 }
 
 // Sum a per-thread refusal count over the CTA and add it to the trusted

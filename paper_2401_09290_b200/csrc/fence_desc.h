@@ -14,7 +14,11 @@ struct FenceDesc {
     uint64_t size;                 // partition size in bytes (check / modulo)
     uint64_t inv;                  // floor(2^64 / size): modulo-mode reciprocal
     unsigned long long *viol;      // trusted counter (outside every partition)
+    uint32_t flags;                // kNoHoist: check / modulo fence every access (no tile-level range test)
+    uint32_t pad_;
 };
+
+constexpr uint32_t kNoHoist = 1u;
 
 // floor(2^64 / s) for s >= 2
 inline uint64_t recip64(uint64_t s) {

@@ -91,12 +91,12 @@ __global__ void __launch_bounds__(kThreads) k_gather1(const __grid_constant__ Fe
                                                       uint64_t table, uint64_t idx, uint64_t nvec, uint32_t tail) {
     uint32_t nv = 0;
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, v0 = c0 + threadIdx.x;
-    if constexpr (MODE == kCheck) {
+    if constexpr (MODE == kCheck || MODE == kModulo) {   // streams hoisted; random table accesses fenced
         const uint64_t cn = chunk_len(nvec, c0);
         if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, out + 16 * c0, 16 * cn))
-            gather_chunk<kNone, kCheck>(fd, out, table, idx, v0, nvec, nv);
+            gather_chunk<kNone, MODE>(fd, out, table, idx, v0, nvec, nv);
         else
-            gather_chunk<kCheck, kCheck>(fd, out, table, idx, v0, nvec, nv);
+            gather_chunk<MODE, MODE>(fd, out, table, idx, v0, nvec, nv);
     } else {
         gather_chunk<MODE, MODE>(fd, out, table, idx, v0, nvec, nv);
     }
@@ -141,6 +141,67 @@ __global__ void __launch_bounds__(kThreads) k_gatherD(const __grid_constant__ Fe
             if (f4.ok(ao)) *reinterpret_cast<uint32_t *>(f4.addr(ao)) = r;
             else nv++;
         }
+    }
+    if constexpr (MODE == kCheck) flush_violations(nv, fd.viol);
+}
+
+// ---------------------------------------------------------------------------
+// K3, D % 4 == 0 (16-byte-aligned rows): embedding rows moved as 128-bit
+// vectors.  Vector e of the output is element group v = e % (D/4) of row
+// i = e / (D/4): out + 16 e <- table + 4 (sext(j_i) D) + 16 v.  Every CTA owns
+// kThreads x kU consecutive output vectors (coalesced stores; a row of D >= 32
+// words is one or more whole 128-byte lines, so DRAM moves only useful bytes).
+// Logical accesses as in the oracle: one index load per row (counted by the
+// row's v == 0 vector), D table loads and D stores per row (4 per vector).
+// ---------------------------------------------------------------------------
+template <int SMODE, int TMODE>
+__device__ __forceinline__ void gatherv_chunk(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t idx,
+                                              uint64_t e0, uint64_t nv_total, uint32_t vpr, uint32_t &nv) {
+    const Fence<SMODE, 4> fi(fd);
+    const Fence<SMODE, 16> fo(fd);
+    const Fence<TMODE, 16> ft(fd);
+    uint4 r[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+        const uint64_t e = e0 + u * kThreads;
+        r[u] = make_uint4(0, 0, 0, 0);
+        if (e < nv_total) {
+            const uint64_t i = nv_total <= 0xFFFFFFFFull ? (uint64_t)((uint32_t)e / vpr) : e / vpr;
+            const uint64_t v = e - i * vpr;
+            const uint64_t ai = idx + 4 * i;
+            int32_t j = 0;
+            if (fi.ok(ai)) j = __ldg(reinterpret_cast<const int32_t *>(fi.addr(ai)));
+            else nv += (v == 0);
+            const uint64_t at = table + (uint64_t)((int64_t)j * (int64_t)vpr * 16) + 16 * v;
+            if (ft.ok(at)) r[u] = __ldcg(reinterpret_cast<const uint4 *>(ft.addr(at)));
+            else nv += 4;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+        const uint64_t e = e0 + u * kThreads;
+        if (e < nv_total) {
+            const uint64_t ao = out + 16 * e;
+            if (fo.ok(ao)) st_out(fo.addr(ao), r[u]);
+            else nv += 4;
+        }
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_gatherV(const __grid_constant__ FenceDesc fd, uint64_t out,
+                                                      uint64_t table, uint64_t idx, uint64_t nv_total, uint32_t vpr) {
+    uint32_t nv = 0;
+    const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, e0 = c0 + threadIdx.x;
+    if constexpr (MODE == kCheck || MODE == kModulo) {   // streams hoisted; table rows fenced
+        const uint64_t cn = chunk_len(nv_total, c0);
+        const uint64_t r0 = c0 / vpr, r1 = (c0 + cn - 1) / vpr;       // rows this CTA touches
+        if (cn && range_in(fd, idx + 4 * r0, 4 * (r1 - r0 + 1)) && range_in(fd, out + 16 * c0, 16 * cn))
+            gatherv_chunk<kNone, MODE>(fd, out, table, idx, e0, nv_total, vpr, nv);
+        else
+            gatherv_chunk<MODE, MODE>(fd, out, table, idx, e0, nv_total, vpr, nv);
+    } else {
+        gatherv_chunk<MODE, MODE>(fd, out, table, idx, e0, nv_total, vpr, nv);
     }
     if constexpr (MODE == kCheck) flush_violations(nv, fd.viol);
 }
@@ -194,12 +255,12 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Fe
                                                       uint64_t idx, uint64_t src, uint64_t nvec, uint32_t tail) {
     uint32_t nv = 0;
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, v0 = c0 + threadIdx.x;
-    if constexpr (MODE == kCheck) {
+    if constexpr (MODE == kCheck || MODE == kModulo) {   // streams hoisted; random RMWs fenced
         const uint64_t cn = chunk_len(nvec, c0);
         if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, src + 16 * c0, 16 * cn))
-            scatter_chunk<kNone, kCheck>(fd, table, idx, src, v0, nvec, nv);
+            scatter_chunk<kNone, MODE>(fd, table, idx, src, v0, nvec, nv);
         else
-            scatter_chunk<kCheck, kCheck>(fd, table, idx, src, v0, nvec, nv);
+            scatter_chunk<MODE, MODE>(fd, table, idx, src, v0, nvec, nv);
     } else {
         scatter_chunk<MODE, MODE>(fd, table, idx, src, v0, nvec, nv);
     }
@@ -234,6 +295,8 @@ cudaError_t gather_t(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t
                      cudaStream_t s, const Geom &g) {
     if (D == 1) {
         k_gather1<MODE><<<chunk_grid(n / 4), kThreads, 0, s>>>(fd, out, table, idx, n / 4, (uint32_t)(n % 4));
+    } else if (D % 4 == 0 && (table | out) % 16 == 0) {
+        k_gatherV<MODE><<<chunk_grid(n * (D / 4)), kThreads, 0, s>>>(fd, out, table, idx, n * (D / 4), D / 4);
     } else {
         static const int bps = blocks_per_sm(k_gatherD<MODE>);
         const uint64_t want = (n * 32 + kThreads - 1) / kThreads, cap = (uint64_t)g.sms * bps;

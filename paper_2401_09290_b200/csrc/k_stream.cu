@@ -62,12 +62,12 @@ __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ Fence
     uint32_t nv = 0;
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
     const uint64_t v0 = c0 + threadIdx.x;
-    if constexpr (MODE == kCheck) {
+    if constexpr (MODE == kCheck || MODE == kModulo) {   // both fences are the identity inside the partition
         const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
         if (cn && range_in(fd, src + 16 * c0, 16 * cn) && range_in(fd, dst + 16 * c0, 16 * cn))
             copy_chunk<kNone>(fd, dst, src, v0, nvec, nv);
         else
-            copy_chunk<kCheck>(fd, dst, src, v0, nvec, nv);
+            copy_chunk<MODE>(fd, dst, src, v0, nvec, nv);
     } else {
         copy_chunk<MODE>(fd, dst, src, v0, nvec, nv);
     }
@@ -126,12 +126,12 @@ __global__ void __launch_bounds__(kThreads) k_saxpy(const __grid_constant__ Fenc
     uint32_t nv = 0;
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
     const uint64_t v0 = c0 + threadIdx.x;
-    if constexpr (MODE == kCheck) {
+    if constexpr (MODE == kCheck || MODE == kModulo) {   // both fences are the identity inside the partition
         const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
         if (cn && range_in(fd, x + 16 * c0, 16 * cn) && range_in(fd, y + 16 * c0, 16 * cn))
             saxpy_chunk<kNone>(fd, alpha, x, y, v0, nvec, nv);
         else
-            saxpy_chunk<kCheck>(fd, alpha, x, y, v0, nvec, nv);
+            saxpy_chunk<MODE>(fd, alpha, x, y, v0, nvec, nv);
     } else {
         saxpy_chunk<MODE>(fd, alpha, x, y, v0, nvec, nv);
     }

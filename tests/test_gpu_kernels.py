@@ -194,7 +194,7 @@ def test_gather_adversarial(arenas, mode, frac):
 
 
 @pytest.mark.parametrize("mode", MODES[1:])
-@pytest.mark.parametrize("D", [2, 3, 33])
+@pytest.mark.parametrize("D", [2, 3, 33, 4, 8, 32, 132])     # D % 4 == 0: 128-bit row path
 def test_gather_rows(arenas, mode, D):
     a, parts, rng = _setup(arenas, seed=9)
     n = 5000 + D
