@@ -53,6 +53,12 @@ struct Fence {
         if constexpr (MODE == kCheck) return (a - base) <= lim && (a & (uint64_t)(W - 1)) == 0;
         else return true;
     }
+    // ok() for an address the caller has proven W-aligned (aligned operand
+    // bases and W-multiple strides): the alignment half of the test is known true
+    __device__ __forceinline__ bool ok_aligned(uint64_t a) const {
+        if constexpr (MODE == kCheck) return (a - base) <= lim;
+        else return true;
+    }
 };
 
 // Check-mode hoisting: true iff every byte of [a, a+len) lies in the

@@ -11,9 +11,10 @@
 // random 32-bit table loads (L1-bypassing, sector-granular), then kU 128-bit
 // output stores.  In check mode the index and output streams are range-tested
 // once per CTA chunk (fence.cuh range_in); the random table accesses are
-// checked one by one.  D > 1 path: one warp per index row, lanes stride over
-// the row; lane 0 loads the index once (one logical access, as in the
-// oracle) and broadcasts it.
+// checked one by one.  D % 4 == 0 with 16-byte-aligned table and output:
+// row slots of 128-bit vectors (k_gatherR below).  Other D > 1: one warp per
+// index row, lanes stride over the row; lane 0 loads the index once (one
+// logical access, as in the oracle) and broadcasts it.
 #include "fence.cuh"
 #include "kernels.h"
 
@@ -147,61 +148,137 @@ __global__ void __launch_bounds__(kThreads) k_gatherD(const __grid_constant__ Fe
 
 // ---------------------------------------------------------------------------
 // K3, D % 4 == 0 (16-byte-aligned rows): embedding rows moved as 128-bit
-// vectors.  Vector e of the output is element group v = e % (D/4) of row
-// i = e / (D/4): out + 16 e <- table + 4 (sext(j_i) D) + 16 v.  Every CTA owns
-// kThreads x kU consecutive output vectors (coalesced stores; a row of D >= 32
-// words is one or more whole 128-byte lines, so DRAM moves only useful bytes).
+// vectors in row slots.  A row of vpr = D/4 vectors is split into tpr = vpr/G
+// slots of G vectors (G = 4, 2 or 1, dividing vpr); slot t of
+// row i moves vectors t + tpr*g (g < G): table + 16 (sext(j_i) vpr + t + tpr g)
+// -> out + 16 (i vpr + t + tpr g).  Consecutive threads take consecutive
+// slots, so every warp instruction covers whole 16-byte pieces of contiguous
+// runs (coalesced); the index load, the row address and the table fence of
+// check / modulo mode are paid once per slot instead of once per vector: a
+// row wholly inside the partition (check) or not wrapping around its end
+// (modulo) needs no per-vector fence (same results, see range_in).  Each
+// thread owns 4/G slots, i.e. 4 vectors (64 B) in flight.  G is chosen so
+// that a row still has >= 8 slots (see gather_t).
 // Logical accesses as in the oracle: one index load per row (counted by the
-// row's v == 0 vector), D table loads and D stores per row (4 per vector).
+// row's t == 0 slot), D table loads and D stores per row (4 per vector).
 // ---------------------------------------------------------------------------
-template <int SMODE, int TMODE>
-__device__ __forceinline__ void gatherv_chunk(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t idx,
-                                              uint64_t e0, uint64_t nv_total, uint32_t vpr, uint32_t &nv) {
+// Row of slot sl without a branch (a branch between the index loads would
+// make the compiler consume each loaded index before the next load issues):
+// a shift when the slots per row are a power of two (P2, dv = log2 tpr),
+// else the reciprocal dv = floor(2^64 / tpr) (tpr >= 3): q = mulhi(sl, dv) is
+// sl / tpr or one less, one predicated add finishes it.
+template <bool P2>
+__device__ __forceinline__ uint64_t row_of(uint64_t sl, uint64_t tpr, uint64_t dv) {
+    if constexpr (P2) {
+        return sl >> dv;
+    } else {
+        uint64_t q = __umul64hi(sl, dv);
+        if (sl - q * tpr >= tpr) q++;
+        return q;
+    }
+}
+
+template <int SMODE, int TMODE, int G, bool P2>
+__device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t idx,
+                                              uint64_t s0, uint64_t nslots, uint32_t tpr32, uint64_t dv,
+                                              uint32_t &nv) {
+    constexpr int S = 4 / G;
     const Fence<SMODE, 4> fi(fd);
     const Fence<SMODE, 16> fo(fd);
     const Fence<TMODE, 16> ft(fd);
-    uint4 r[kU];
+    const uint64_t tpr = tpr32, vpr = tpr * G, rowbytes = 16 * vpr;
+    // Every address here is aligned by construction (idx 4-, table and out
+    // 16-aligned: gather_t and the API check), hence ok_aligned.
+    // Phases keep every load of a kind in flight together: the fence's rare
+    // per-vector path is a branch, and a branch between two loads would
+    // serialise their latencies.
+    bool live[S];
+    int32_t j[S];
+    uint64_t ov[S], tv[S];
 #pragma unroll
-    for (int u = 0; u < kU; u++) {
-        const uint64_t e = e0 + u * kThreads;
-        r[u] = make_uint4(0, 0, 0, 0);
-        if (e < nv_total) {
-            const uint64_t i = nv_total <= 0xFFFFFFFFull ? (uint64_t)((uint32_t)e / vpr) : e / vpr;
-            const uint64_t v = e - i * vpr;
-            const uint64_t ai = idx + 4 * i;
-            int32_t j = 0;
-            if (fi.ok(ai)) j = __ldg(reinterpret_cast<const int32_t *>(fi.addr(ai)));
-            else nv += (v == 0);
-            const uint64_t at = table + (uint64_t)((int64_t)j * (int64_t)vpr * 16) + 16 * v;
-            if (ft.ok(at)) r[u] = __ldcg(reinterpret_cast<const uint4 *>(ft.addr(at)));
-            else nv += 4;
+    for (int k = 0; k < S; k++) {                       // 1. index loads (predicated, no branch:
+        const uint64_t sl = s0 + (uint64_t)k * kThreads; //    a branch would serialise them)
+        live[k] = sl < nslots;
+        const uint64_t i = row_of<P2>(sl, tpr, dv);
+        const uint64_t t = sl - i * tpr;
+        const uint64_t ai = idx + 4 * i;
+        const bool oki = live[k] && fi.ok_aligned(ai);
+        j[k] = 0;
+        if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fi.addr(ai)));
+        if (live[k] && !oki) nv += (t == 0);
+        ov[k] = out + 16 * (i * vpr + t);
+        tv[k] = 16 * t;
+    }
+    uint64_t at[S][G];
+    bool ok[S][G];
+#pragma unroll
+    for (int k = 0; k < S; k++) {                       // 2. fenced table addresses (ALU only)
+        const uint64_t rt = table + (uint64_t)((int64_t)j[k] * (int64_t)rowbytes) + tv[k];   // vector g = 0
+        bool whole = false;                             // every vector of the slot in / unwrapped
+        uint64_t fr = rt;
+        if constexpr (G > 1 && TMODE == kCheck) {
+            whole = range_in(fd, rt, 16 * tpr * (G - 1) + 16);
+        } else if constexpr (G > 1 && TMODE == kModulo) {
+            fr = ft.addr(rt);                           // rt is 16-aligned: fr - base = (rt - base) mod size
+            const uint64_t span = 16 * tpr * (G - 1) + 16;
+            whole = !(fd.flags & kNoHoist) && span <= fd.size && fr - fd.base <= fd.size - span;
+        }
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            const uint64_t a = rt + 16 * tpr * g;
+            if constexpr (TMODE == kNone || TMODE == kMask) {
+                at[k][g] = ft.addr(a);
+                ok[k][g] = true;
+            } else if (whole) {
+                at[k][g] = fr + 16 * tpr * g;
+                ok[k][g] = true;
+            } else {
+                at[k][g] = ft.addr(a);
+                ok[k][g] = ft.ok_aligned(a);
+            }
+        }
+    }
+    uint4 r[S][G];
+#pragma unroll
+    for (int k = 0; k < S; k++) {                       // 3. table loads
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            r[k][g] = make_uint4(0, 0, 0, 0);
+            if (live[k] && ok[k][g]) r[k][g] = __ldcg(reinterpret_cast<const uint4 *>(at[k][g]));
+            if (live[k] && !ok[k][g]) nv += 4;
         }
     }
 #pragma unroll
-    for (int u = 0; u < kU; u++) {
-        const uint64_t e = e0 + u * kThreads;
-        if (e < nv_total) {
-            const uint64_t ao = out + 16 * e;
-            if (fo.ok(ao)) st_out(fo.addr(ao), r[u]);
-            else nv += 4;
+    for (int k = 0; k < S; k++) {                       // 4. output stores
+        if (live[k]) {
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                const uint64_t ao = ov[k] + 16 * tpr * g;
+                if (fo.ok_aligned(ao)) st_out(fo.addr(ao), r[k][g]);
+                else nv += 4;
+            }
         }
     }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_gatherV(const __grid_constant__ FenceDesc fd, uint64_t out,
-                                                      uint64_t table, uint64_t idx, uint64_t nv_total, uint32_t vpr) {
+template <int MODE, int G, bool P2>
+__global__ void __launch_bounds__(kThreads, 6) k_gatherR(const __grid_constant__ FenceDesc fd, uint64_t out,
+                                                      uint64_t table, uint64_t idx, uint64_t nslots, uint32_t tpr,
+                                                      uint64_t dv) {
+    constexpr uint64_t ch = (uint64_t)kThreads * (4 / G);
     uint32_t nv = 0;
-    const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, e0 = c0 + threadIdx.x;
-    if constexpr (MODE == kCheck || MODE == kModulo) {   // streams hoisted; table rows fenced
-        const uint64_t cn = chunk_len(nv_total, c0);
-        const uint64_t r0 = c0 / vpr, r1 = (c0 + cn - 1) / vpr;       // rows this CTA touches
-        if (cn && range_in(fd, idx + 4 * r0, 4 * (r1 - r0 + 1)) && range_in(fd, out + 16 * c0, 16 * cn))
-            gatherv_chunk<kNone, MODE>(fd, out, table, idx, e0, nv_total, vpr, nv);
+    const uint64_t c0 = (uint64_t)blockIdx.x * ch, s0 = c0 + threadIdx.x;
+    if constexpr (MODE == kCheck || MODE == kModulo) {   // streams hoisted per CTA; table rows per slot
+        const uint64_t cn = nslots > c0 ? (nslots - c0 < ch ? nslots - c0 : ch) : 0;
+        const uint64_t r0 = row_of<P2>(c0, tpr, dv);                   // rows this CTA touches
+        const uint64_t nr = cn ? row_of<P2>(c0 + cn - 1, tpr, dv) - r0 + 1 : 0;
+        const uint64_t rb = 16ull * tpr * G;
+        if (cn && range_in(fd, idx + 4 * r0, 4 * nr) && range_in(fd, out + rb * r0, rb * nr))
+            gatherr_chunk<kNone, MODE, G, P2>(fd, out, table, idx, s0, nslots, tpr, dv, nv);
         else
-            gatherv_chunk<MODE, MODE>(fd, out, table, idx, e0, nv_total, vpr, nv);
+            gatherr_chunk<MODE, MODE, G, P2>(fd, out, table, idx, s0, nslots, tpr, dv, nv);
     } else {
-        gatherv_chunk<MODE, MODE>(fd, out, table, idx, e0, nv_total, vpr, nv);
+        gatherr_chunk<MODE, MODE, G, P2>(fd, out, table, idx, s0, nslots, tpr, dv, nv);
     }
     if constexpr (MODE == kCheck) flush_violations(nv, fd.viol);
 }
@@ -296,7 +373,25 @@ cudaError_t gather_t(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t
     if (D == 1) {
         k_gather1<MODE><<<chunk_grid(n / 4), kThreads, 0, s>>>(fd, out, table, idx, n / 4, (uint32_t)(n % 4));
     } else if (D % 4 == 0 && (table | out) % 16 == 0) {
-        k_gatherV<MODE><<<chunk_grid(n * (D / 4)), kThreads, 0, s>>>(fd, out, table, idx, n * (D / 4), D / 4);
+        // G: the most vectors per slot that still leaves >= 8 slots (128 B,
+        // one full line) per row per warp instruction -- narrower pieces
+        // multiply the L2 requests per byte (measured: D = 8 at G = 2 and
+        // D = 32 at G = 4 lose 35% / 10%)
+        const uint32_t vpr = D / 4;
+        const uint32_t G = (vpr % 4 == 0 && vpr >= 32) ? 4 : (vpr % 2 == 0 && vpr >= 16) ? 2 : 1, tpr = vpr / G;
+        const uint64_t nslots = n * tpr, per_cta = (uint64_t)kThreads * (4 / G);
+        const unsigned grid = (unsigned)(nslots ? (nslots + per_cta - 1) / per_cta : 1);
+        if ((tpr & (tpr - 1)) == 0) {
+            const uint64_t sh = (uint64_t)__builtin_ctz(tpr);
+            if (G == 4) k_gatherR<MODE, 4, true><<<grid, kThreads, 0, s>>>(fd, out, table, idx, nslots, tpr, sh);
+            else if (G == 2) k_gatherR<MODE, 2, true><<<grid, kThreads, 0, s>>>(fd, out, table, idx, nslots, tpr, sh);
+            else k_gatherR<MODE, 1, true><<<grid, kThreads, 0, s>>>(fd, out, table, idx, nslots, tpr, sh);
+        } else {
+            const uint64_t inv = recip64(tpr);          // tpr >= 3
+            if (G == 4) k_gatherR<MODE, 4, false><<<grid, kThreads, 0, s>>>(fd, out, table, idx, nslots, tpr, inv);
+            else if (G == 2) k_gatherR<MODE, 2, false><<<grid, kThreads, 0, s>>>(fd, out, table, idx, nslots, tpr, inv);
+            else k_gatherR<MODE, 1, false><<<grid, kThreads, 0, s>>>(fd, out, table, idx, nslots, tpr, inv);
+        }
     } else {
         static const int bps = blocks_per_sm(k_gatherD<MODE>);
         const uint64_t want = (n * 32 + kThreads - 1) / kThreads, cap = (uint64_t)g.sms * bps;

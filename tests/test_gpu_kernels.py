@@ -194,7 +194,7 @@ def test_gather_adversarial(arenas, mode, frac):
 
 
 @pytest.mark.parametrize("mode", MODES[1:])
-@pytest.mark.parametrize("D", [2, 3, 33, 4, 8, 32, 132])     # D % 4 == 0: 128-bit row path
+@pytest.mark.parametrize("D", [2, 3, 33, 4, 8, 32, 64, 128, 132, 136])     # D % 4 == 0: 128-bit row slots
 def test_gather_rows(arenas, mode, D):
     a, parts, rng = _setup(arenas, seed=9)
     n = 5000 + D
@@ -205,6 +205,33 @@ def test_gather_rows(arenas, mode, D):
          lambda p: a.gather(p.id, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, n, D),
          lambda m, p: oracle.gather(m, p.base, p.size, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, n, D),
          None if mode == "mask" else len(pos) * D)
+
+
+@pytest.mark.parametrize("mode", ["mask", "check", "modulo"])
+@pytest.mark.parametrize("D", [8, 36, 64, 128, 136])    # row-slot widths G = 1, 1, 2, 4, 2
+def test_gather_rows_straddle(arenas, mode, D):
+    """Rows that straddle the partition end or base: the row-slot kernel's
+    per-row fast path must not apply, each 16-byte vector is fenced alone
+    (check: the outside vectors refused; mask / modulo: only they wrap)."""
+    a, parts, rng = _setup(arenas, seed=19)
+    n = 3000 + D
+    tab_off = 48                                    # 16-aligned, not row-aligned
+    j = rng.integers(0, TAB_N // D - 1, n, dtype=np.int64)
+    j_hi = (PART - tab_off) // (4 * D)              # row start inside, end past the partition end
+    assert tab_off + 4 * D * j_hi < PART < tab_off + 4 * D * (j_hi + 1)
+    pos = synth.planted_positions(rng, n, 64)
+    j[pos[::2]] = j_hi
+    j[pos[1::2]] = -1                               # row ends at base + 48: straddles the base for D > 12
+    j = j.astype(np.int32)
+    upload(parts[1].base + IDX_OFF, j)
+    _, c = _run(a, parts, 1, mode,
+                lambda p: a.gather(p.id, mode, p.base + OUT_OFF, p.base + tab_off, p.base + IDX_OFF, n, D),
+                lambda m, p: oracle.gather(m, p.base, p.size, mode, p.base + OUT_OFF, p.base + tab_off,
+                                           p.base + IDX_OFF, n, D))
+    if mode == "check":
+        out_hi = 4 * D - (PART - tab_off - 4 * D * j_hi)          # words past the end per j_hi row
+        out_lo = max(0, 4 * D - tab_off) // 4                      # words below the base per j = -1 row
+        assert c.violations == 32 * (out_hi // 4 + out_lo)
 
 
 @pytest.mark.parametrize("mode", MODES)

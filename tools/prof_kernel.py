@@ -1,8 +1,10 @@
 """Launch one fenced kernel a few times on a single tenant partition (for ncu).
 
   python tools/prof_kernel.py --kind saxpy --mode mask [--reps 3]
+  python tools/prof_kernel.py --kind gatherrows --D 32 --mode check
 Sizes are the bench's per-tenant sizes (4 GiB tensors; C3 gather; 8192^3 GEMM;
-32768^2 stencil) in a 16 GiB partition.
+32768^2 stencil; kernel_bench's 1 GiB of gathered D-word rows) in a 16 GiB
+partition.
 """
 import argparse
 import os
@@ -22,6 +24,7 @@ def main():
     ap.add_argument("--kind", default="saxpy")
     ap.add_argument("--mode", default="mask")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--D", type=int, default=32, help="row width (words) for --kind gatherrows")
     a = ap.parse_args()
     ar = g.Arena(0, 1 << 34)
     p = ar.partition_alloc(1 << 34)
@@ -35,6 +38,11 @@ def main():
         pos = torch.randperm(1 << 26, generator=gen, device="cuda:0")[: (1 << 26) // 100]
         idx[pos] = torch.randint(-2**31, 0, (pos.numel(),), generator=gen, device="cuda:0", dtype=torch.int32)
         devmem.view(b, 1 << 29, torch.int32).random_(generator=gen)
+    if a.kind == "gatherrows":
+        T = 1 << 29
+        rows, n_rows = T // a.D, GiB // (4 * a.D)
+        devmem.view(b, T, torch.int32).random_(generator=gen)
+        devmem.view(b + 2 * GiB + GiB // 2, n_rows, torch.int32).random_(0, rows, generator=gen)
     for _ in range(a.reps):
         if a.kind == "copy":
             ar.copy(p.id, a.mode, b + 4 * GiB, b, 4 * GiB)
@@ -42,6 +50,8 @@ def main():
             ar.saxpy(p.id, a.mode, 1.5, b + 8 * GiB, b + 12 * GiB, 1 << 30)
         elif a.kind == "gather":
             ar.gather(p.id, a.mode, b + 2 * GiB + GiB // 4, b, b + 2 * GiB, 1 << 26)
+        elif a.kind == "gatherrows":
+            ar.gather(p.id, a.mode, b + 3 * GiB, b, b + 2 * GiB + GiB // 2, n_rows, a.D)
         elif a.kind == "scatter":
             ar.scatter(p.id, a.mode, b, b + 2 * GiB, b + 2 * GiB + GiB // 4, 1 << 26)
         elif a.kind == "stencil":
