@@ -337,8 +337,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-        const __grid_constant__ CUtensorMap tmC, uint32_t K, uint32_t tm, uint32_t tn, uint32_t group,
-        uint32_t l2hint) {
+        const __grid_constant__ CUtensorMap tmC, uint32_t K, uint32_t tm, uint32_t tn, uint32_t group) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *epi = smem + STAGES2 * STAGE2_BYTES;                  // C staging, 16 KB
@@ -380,22 +379,6 @@ k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
         // ---------------- TMA producer (both CTAs) ----------------
         uint32_t it = 0;
         bool alive = true;
-        // L2 eviction priority per operand (l2hint 1: A panels evict_last, B
-        // evict_first -- within a raster group the A panels are the reused ones)
-        uint64_t polA, polB;
-        if (l2hint == 1) {
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(polA));
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(polB));
-        } else if (l2hint == 2) {
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(polA));
-            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(polB));
-        } else if (l2hint == 3) {
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 0.5;" : "=l"(polA));
-            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(polB));
-        } else {
-            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(polA));
-            polB = polA;
-        }
         for (uint32_t t = pair; t < ntiles && alive; t += npairs) {
             uint32_t mb, nb;
             tile_coords(t, tm, tn, group, mb, nb);
@@ -414,13 +397,11 @@ k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
                 const int kc = (int)(kb * BK);
                 asm volatile(
                     "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                    ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(sa), "l"(&tmA), "r"(fb), "r"(kc),
-                    "r"(row_a), "l"(polA)
+                    " [%0], [%1, {%3, %4}], [%2];" ::"r"(sa), "l"(&tmA), "r"(fb), "r"(kc), "r"(row_a)
                     : "memory");
                 asm volatile(
                     "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                    ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(sb), "l"(&tmB), "r"(fb), "r"(kc),
-                    "r"(row_b), "l"(polB)
+                    " [%0], [%1, {%3, %4}], [%2];" ::"r"(sb), "l"(&tmB), "r"(fb), "r"(kc), "r"(row_b)
                     : "memory");
             }
         }
@@ -624,10 +605,6 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
         const int v = e ? atoi(e) : 0;
         return (uint32_t)(v > 0 ? v : GROUP_M);
     }();
-    static const uint32_t l2hint = [] {                // TMA L2 eviction priorities; tuning knob
-        const char *e = getenv("GD_GEMM_L2HINT");
-        return (uint32_t)(e ? atoi(e) : 0);
-    }();
     if (rC >= 2 * BM && !force1 && g.sms >= 2) {
         // 2-SM path: B staged in N halves per CTA
         CUtensorMap tmB2;
@@ -636,7 +613,7 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
         const uint32_t tm = (uint32_t)((rC + 2 * BM - 1) / (2 * BM)), tn = (N + BN - 1) / BN;
         const uint32_t ntiles = tm * tn, pairs_max = (uint32_t)g.sms / 2;
         const uint32_t grid = 2 * (ntiles < pairs_max ? ntiles : pairs_max);
-        k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, tmC, K, tm, tn, group, l2hint);
+        k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, tmC, K, tm, tn, group);
         return cuda_status(cudaGetLastError());
     }
     if (!make_map(&tmB, Bf, K, rB, ldB, BN)) return GD_ERR_UNSUPPORTED;
