@@ -72,8 +72,9 @@ def main():
                     print(f"   {k:72s} {m['value']:>16.4f} {m['unit']}")
             if "dram__bytes_read.sum" in d:
                 rd, wr = to_bytes(d["dram__bytes_read.sum"]), to_bytes(d["dram__bytes_write.sum"])
-                mm = re.search(r"(k_[a-z0-9]+)<(\d)>", name)
-                key = f"{mm.group(1)}<{mm.group(2)}>" if mm else re.sub(r"\(.*", "", name)
+                mm = re.search(r"(k_[A-Za-z0-9]+)<([\d, ]+)>", name)
+                key = (f"{mm.group(1)}<{mm.group(2).replace(' ', '')}>" if mm
+                       else re.sub(r"^.*::", "", re.sub(r"\(.*", "", name)))
                 traffic[key] = rd + wr
                 print(f"   traffic (dram read+write) = {rd + wr:.4e} B")
     if out:
