@@ -22,8 +22,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
-NONE, MASK, CHECK, MODULO = 0, 1, 2, 3
-MODES = {"none": NONE, "mask": MASK, "check": CHECK, "modulo": MODULO}
+NONE, MASK, CHECK, MODULO, MASK_COUNT, CLAMP = 0, 1, 2, 3, 4, 5
+MODES = {"none": NONE, "mask": MASK, "check": CHECK, "modulo": MODULO, "maskcount": MASK_COUNT, "clamp": CLAMP}
 
 
 class OrCtx(ctypes.Structure):
@@ -74,6 +74,12 @@ def lib():
         L.or_fence_modulo.argtypes = [u64, u64, u64, u32]
         L.or_fence_modulo_n.argtypes = [ctypes.c_void_p, u64, u64, u64, u32, ctypes.c_void_p]
         L.or_fence_modulo_n.restype = None
+        L.or_fence_clamp.restype = u64
+        L.or_fence_clamp.argtypes = [u64, u64, u64, u32]
+        L.or_fence_clamp_n.argtypes = [ctypes.c_void_p, u64, u64, u64, u32, ctypes.c_void_p]
+        L.or_fence_clamp_n.restype = None
+        L.or_counted.restype = i32
+        L.or_counted.argtypes = [P, u64, u32]
         L.or_check_ok.restype = i32
         L.or_check_ok.argtypes = [u64, u64, u64, u32]
         L.or_check_range.restype = i32
@@ -111,6 +117,10 @@ def fence_modulo(a: int, base: int, size: int, w: int = 1) -> int:
     return lib().or_fence_modulo(a & (2**64 - 1), base, size, w)
 
 
+def fence_clamp(a: int, base: int, size: int, w: int = 1) -> int:
+    return lib().or_fence_clamp(a & (2**64 - 1), base, size, w)
+
+
 def fence_mask(a: int, base: int, size: int, w: int = 1) -> int:
     return lib().or_fence_mask(a & (2**64 - 1), base, size, w)
 
@@ -134,6 +144,13 @@ def fence_modulo_n(a: np.ndarray, base: int, size: int, w: int = 1) -> np.ndarra
     a = np.ascontiguousarray(a, dtype=np.uint64)
     out = np.empty_like(a)
     lib().or_fence_modulo_n(a.ctypes.data, a.size, base, size, w, out.ctypes.data)
+    return out
+
+
+def fence_clamp_n(a: np.ndarray, base: int, size: int, w: int = 1) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    out = np.empty_like(a)
+    lib().or_fence_clamp_n(a.ctypes.data, a.size, base, size, w, out.ctypes.data)
     return out
 
 

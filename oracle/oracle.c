@@ -69,10 +69,20 @@ int or_check_range(uint64_t base, uint64_t size, uint64_t addr, uint64_t len) {
     return 1;
 }
 
+uint64_t or_fence_clamp(uint64_t a, uint64_t base, uint64_t size, uint32_t w) {
+    /* north_star: check mode may "compare, clamp and set a violation flag".
+     * Clamp to the partition's w-aligned addresses [base, base+size-w].     */
+    uint64_t last = base + size - w;
+    if (a < base) return base;
+    if (a > last) return last;
+    return a - a % w;                        /* base is w-aligned: stays >= base */
+}
+
 uint64_t or_resolve(const or_ctx *c, uint64_t a, uint32_t w, int *ok) {
     *ok = 1;
-    if (c->mode == OR_MASK) return or_fence_mask(a, c->base, c->size, w);
+    if (c->mode == OR_MASK || c->mode == OR_MASK_COUNT) return or_fence_mask(a, c->base, c->size, w);
     if (c->mode == OR_MODULO) return or_fence_modulo(a, c->base, c->size, w);
+    if (c->mode == OR_CLAMP) return or_fence_clamp(a, c->base, c->size, w);
     if (c->mode == OR_CHECK) {
         if (!or_check_ok(a, c->base, c->size, w)) {
             *ok = 0;
@@ -81,6 +91,17 @@ uint64_t or_resolve(const or_ctx *c, uint64_t a, uint32_t w, int *ok) {
         return a;
     }
     return a;
+}
+
+int or_counted(const or_ctx *c, uint64_t a, uint32_t w) {
+    if (c->mode == OR_CHECK || c->mode == OR_MASK_COUNT || c->mode == OR_CLAMP)
+        return !or_check_ok(a, c->base, c->size, w);
+    return 0;
+}
+
+void or_fence_clamp_n(const uint64_t *a, uint64_t n, uint64_t base,
+                      uint64_t size, uint32_t w, uint64_t *out) {
+    for (uint64_t i = 0; i < n; i++) out[i] = or_fence_clamp(a[i], base, size, w);
 }
 
 void or_fence_mask_n(const uint64_t *a, uint64_t n, uint64_t base,
@@ -112,10 +133,8 @@ static uint8_t *fenced(or_ctx *c, uint64_t a, uint32_t w) {
     int ok;
     c->accesses++;
     uint64_t r = or_resolve(c, a, w, &ok);
-    if (!ok) {
-        c->violations++;
-        return NULL;
-    }
+    if (or_counted(c, a, w)) c->violations++;
+    if (!ok) return NULL;
     return mem_at(c, r, w);
 }
 
@@ -227,8 +246,12 @@ uint64_t or_desc_rows(const or_ctx *c, uint64_t p, uint64_t rows,
         /* the descriptor's global address is fenced like a 16-byte access
          * (tensor-map addresses must be 16-byte aligned)                   */
         pf = or_fence_mask(p, c->base, c->size, 16);
+    } else if (c->mode == OR_MASK_COUNT) {
+        pf = or_fence_mask(p, c->base, c->size, 16);
     } else if (c->mode == OR_MODULO) {
         pf = or_fence_modulo(p, c->base, c->size, 16);
+    } else if (c->mode == OR_CLAMP) {
+        pf = or_fence_clamp(p, c->base, c->size, 16);
     } else {
         /* check: the start must itself be a legal 16-byte-aligned address */
         if (!or_check_ok(p, c->base, c->size, 16)) return 0;
@@ -265,8 +288,16 @@ void or_gemm(or_ctx *c, uint64_t C, uint64_t A, uint64_t B, uint32_t M,
     uint64_t rA = or_desc_rows(c, A, M, 2ull * K, 2ull * lda, &Af);
     uint64_t rB = or_desc_rows(c, B, N, 2ull * K, 2ull * ldb, &Bf);
     uint64_t rC = or_desc_rows(c, C, M, 2ull * N, 2ull * ldc, &Cf);
-    if (c->mode == OR_CHECK)
-        c->violations += (M - rA) + (N - rB) + (M - rC);
+    if (c->mode == OR_CHECK || c->mode == OR_MASK_COUNT || c->mode == OR_CLAMP) {
+        /* counted as check mode would refuse them: rows of each operand that
+         * are not wholly inside the partition at their unfenced address    */
+        or_ctx chk = *c;
+        uint64_t pf;
+        chk.mode = OR_CHECK;
+        c->violations += (M - or_desc_rows(&chk, A, M, 2ull * K, 2ull * lda, &pf)) +
+                         (N - or_desc_rows(&chk, B, N, 2ull * K, 2ull * ldb, &pf)) +
+                         (M - or_desc_rows(&chk, C, M, 2ull * N, 2ull * ldc, &pf));
+    }
 
     double *arow = (double *)malloc(sizeof(double) * (K ? K : 1));
     double *brow = (double *)malloc(sizeof(double) * (K ? K : 1));

@@ -31,7 +31,14 @@ extern "C" {
 /* Fence modes: none = native kernel ("issues a native kernel"),
  * mask = address fencing with bitwise operations,
  * check = address checking.          */
-enum { OR_NONE = 0, OR_MASK = 1, OR_CHECK = 2, OR_MODULO = 3 };
+enum { OR_NONE = 0, OR_MASK = 1, OR_CHECK = 2, OR_MODULO = 3, OR_MASK_COUNT = 4, OR_CLAMP = 5 };
+/* OR_MASK_COUNT: mask mode plus detection ("an optional
+ *   GD_FLAG_COUNT adds detection"): the access goes where the mask fence puts
+ *   it and is counted when the check predicate refuses it.
+ * OR_CLAMP: north_star's check mode "compare, clamp and set a violation
+ *   flag" (the GD_CHECK_SATURATE variant): the access goes
+ *   to the nearest w-aligned address of the partition at or below it
+ *   (or_fence_clamp) and is counted when the check predicate refuses it.   */
 
 /* One simulated tenant launch context.
  *   va, len, bytes : the simulated device memory; byte bytes[k] stands for
@@ -39,10 +46,12 @@ enum { OR_NONE = 0, OR_MASK = 1, OR_CHECK = 2, OR_MODULO = 3 };
  *   base, size     : the tenant's partition ("the base address,
  *                    and the partition size"); size is a power of two and
  *                    base is size-aligned.
- *   mode           : OR_NONE / OR_MASK / OR_CHECK.
+ *   mode           : OR_NONE / OR_MASK / OR_CHECK / OR_MODULO / OR_MASK_COUNT /
+ *                    OR_CLAMP.
  * Outputs (accumulated, caller zeroes them):
- *   violations     : check-mode accesses that were refused (one per logical
- *                    access).
+ *   violations     : accesses outside the partition in the counting modes
+ *                    (check: refused; mask-count, clamp: performed at the
+ *                    fenced address), one per logical access (§8(c) A1).
  *   faults         : accesses whose final address lies outside the simulated
  *                    memory; they are skipped ("DeviceFault").
  *   accesses       : logical accesses attempted.                               */
@@ -79,9 +88,16 @@ int or_check_ok(uint64_t a, uint64_t base, uint64_t size, uint32_t w);
  * [addr, addr+len) inside [base, base+size) with no 64-bit wraparound;
  * len = 0 is allowed iff base <= addr <= base+size.                          */
 int or_check_range(uint64_t base, uint64_t size, uint64_t addr, uint64_t len);
+/* Clamp fence: the largest w-aligned address x of the partition with x <= a,
+ * or base when there is none: base for a < base, base+size-w for
+ * a > base+size-w, a rounded down to w otherwise (north_star "clamp").    */
+uint64_t or_fence_clamp(uint64_t a, uint64_t base, uint64_t size, uint32_t w);
 /* The address a fenced access really touches in ctx's mode, or 0 with *ok=0
  * when check mode refuses it.  Does not touch memory or counters.           */
 uint64_t or_resolve(const or_ctx *c, uint64_t a, uint32_t w, int *ok);
+/* 1 when the access counts as a violation in ctx's mode: check, mask-count
+ * and clamp modes count exactly the accesses the check predicate refuses.   */
+int or_counted(const or_ctx *c, uint64_t a, uint32_t w);
 /* Element-wise loops over the two functions above (brute-force pins only).   */
 void or_fence_mask_n(const uint64_t *a, uint64_t n, uint64_t base,
                      uint64_t size, uint32_t w, uint64_t *out);
@@ -89,6 +105,8 @@ void or_check_ok_n(const uint64_t *a, uint64_t n, uint64_t base,
                    uint64_t size, uint32_t w, uint8_t *out);
 void or_fence_modulo_n(const uint64_t *a, uint64_t n, uint64_t base,
                        uint64_t size, uint32_t w, uint64_t *out);
+void or_fence_clamp_n(const uint64_t *a, uint64_t n, uint64_t base,
+                      uint64_t size, uint32_t w, uint64_t *out);
 
 /* ---- simulated kernels -------------------------------- */
 /* copy: 16-byte units, then the byte tail.                                   */
