@@ -67,9 +67,24 @@ typedef enum {
  *          parameter holding the 1/partition_size").  Needs no
  *          alignment and no power-of-two size: it is the mode for exact-size
  *          partitions (gd_partition_alloc_exact).  Nothing is detected.
- *  MASK requires a power-of-two, size-aligned partition (GD_ERR_NOT_POW2
- *  otherwise); NONE, CHECK and MODULO take any partition.      */
-typedef enum { GD_MODE_NONE = 0, GD_MODE_MASK = 1, GD_MODE_CHECK = 2, GD_MODE_MODULO = 3 } gd_mode;
+ *  MASK_COUNT: MASK plus detection ("an optional
+ *          GD_FLAG_COUNT adds detection"): every access goes where MASK puts
+ *          it, and each access CHECK would refuse is counted.
+ *  CLAMP : north_star's check mode "compare, clamp and set a violation flag"
+ *          (reading A1's saturating variant): the access goes to the largest
+ *          w-aligned address of the partition at or below it (the base when
+ *          there is none) and each access CHECK would refuse is counted.
+ *          Every out-of-partition store lands on an edge word, so results
+ *          are deterministic only on inputs whose clamped stores do not
+ *          collide (reading R-race).
+ *  MASK and MASK_COUNT require a power-of-two, size-aligned partition
+ *  (GD_ERR_NOT_POW2 otherwise); the others take any partition.
+ *  Counted accesses (CHECK, MASK_COUNT, CLAMP) are equal in number for the
+ *  same launch: one per logical access outside the partition.               */
+typedef enum {
+    GD_MODE_NONE = 0, GD_MODE_MASK = 1, GD_MODE_CHECK = 2, GD_MODE_MODULO = 3,
+    GD_MODE_MASK_COUNT = 4, GD_MODE_CLAMP = 5
+} gd_mode;
 
 /* Kernel kinds (index of the per-kind statistics).                            */
 typedef enum {

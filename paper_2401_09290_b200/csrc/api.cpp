@@ -482,12 +482,13 @@ namespace gd {
 gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry, bool account, uint64_t *bytes_out,
                    uint64_t *flops_out) {
     if (!a) return GD_ERR_INVALID_ARG;
-    if (w.mode > GD_MODE_MODULO || w.kind >= GD_NUM_KINDS) return GD_ERR_INVALID_ARG;
+    if (w.mode > GD_MODE_CLAMP || w.kind >= GD_NUM_KINDS) return GD_ERR_INVALID_ARG;
     uint64_t base, size;
     gd_status st = snapshot(a, w.tenant, &base, &size);
     if (st != GD_OK) return st;
     // mask fencing needs a power-of-two, size-aligned partition
-    if (w.mode == GD_MODE_MASK && ((size & (size - 1)) || (base & (size - 1)))) return GD_ERR_NOT_POW2;
+    if ((w.mode == GD_MODE_MASK || w.mode == GD_MODE_MASK_COUNT) && ((size & (size - 1)) || (base & (size - 1))))
+        return GD_ERR_NOT_POW2;
 
     uint64_t bytes = 0, flops = 0, t;
     bool empty = false;

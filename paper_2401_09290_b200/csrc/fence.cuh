@@ -21,6 +21,12 @@
 //           PAPER.md:175 ("partition base and ending addresses"), 236; A1, A2.
 //           A refused load yields 0, a refused store/atomic is dropped, and
 //           the refusal is counted (aggregated per thread, then per CTA).
+//   MASK_COUNT: the mask fence, plus a count of the accesses the check
+//           predicate refuses ("GD_FLAG_COUNT").
+//   CLAMP : north_star's "compare, clamp and set a violation flag" (A1's
+//           saturating variant): the access goes to the largest w-aligned
+//           address of the partition at or below it (base when there is
+//           none) and is counted when the check predicate refuses it.
 //   NONE  : identity (the unfenced twin, "native kernel").
 #pragma once
 #include <cstdint>
@@ -35,37 +41,109 @@ struct Fence {
     uint64_t base, keep, size, inv, lim;
     __device__ __forceinline__ explicit Fence(const FenceDesc &fd)
         : base(fd.base), keep(fd.mask & ~(uint64_t)(W - 1)), size(fd.size), inv(fd.inv), lim(fd.size - W) {}
-    // address the access really uses (MASK / MODULO: fenced; CHECK / NONE: unchanged)
+    // address the access really uses (MASK / MODULO / CLAMP: fenced; CHECK / NONE: unchanged)
     __device__ __forceinline__ uint64_t addr(uint64_t a) const {
-        if constexpr (MODE == kMask) {
+        if constexpr (MODE == kMask || MODE == kMaskCount) {
             return (a & keep) | base;
         } else if constexpr (MODE == kModulo) {
             const uint64_t off = a - base;
             uint64_t r = off - __umul64hi(off, inv) * size;
             if (r >= size) r -= size;
             return base + (r & ~(uint64_t)(W - 1));
+        } else if constexpr (MODE == kClamp) {
+            const uint64_t down = a & ~(uint64_t)(W - 1);            // base is W-aligned
+            return a < base ? base : (a - base > lim ? base + lim : down);
         } else {
             return a;
         }
     }
+    // the check predicate: every byte in the partition, a W-aligned
+    __device__ __forceinline__ bool inside(uint64_t a) const {
+        return (a - base) <= lim && (a & (uint64_t)(W - 1)) == 0;
+    }
     // may the access be performed?
     __device__ __forceinline__ bool ok(uint64_t a) const {
-        if constexpr (MODE == kCheck) return (a - base) <= lim && (a & (uint64_t)(W - 1)) == 0;
+        if constexpr (MODE == kCheck) return inside(a);
         else return true;
     }
-    // ok() for an address the caller has proven W-aligned (aligned operand
-    // bases and W-multiple strides): the alignment half of the test is known true
+    // ok(), and add k to the thread's count when the mode counts this access
+    __device__ __forceinline__ bool go(uint64_t a, uint32_t &nv, uint32_t k) const {
+        if constexpr (MODE == kCheck) {
+            const bool o = inside(a);
+            if (!o) nv += k;
+            return o;
+        } else if constexpr (counts(MODE)) {
+            if (!inside(a)) nv += k;
+            return true;
+        } else {
+            return true;
+        }
+    }
+    // ok() / go() for an address the caller has proven W-aligned (aligned
+    // operand bases and W-multiple strides): the alignment half of the test is known true
     __device__ __forceinline__ bool ok_aligned(uint64_t a) const {
         if constexpr (MODE == kCheck) return (a - base) <= lim;
         else return true;
     }
+    __device__ __forceinline__ bool go_aligned(uint64_t a, uint32_t &nv, uint32_t k) const {
+        if constexpr (MODE == kCheck) {
+            const bool o = (a - base) <= lim;
+            if (!o) nv += k;
+            return o;
+        } else if constexpr (counts(MODE)) {
+            if ((a - base) > lim) nv += k;
+            return true;
+        } else {
+            return true;
+        }
+    }
+    // CLAMP, for a 16-byte vector of four logical 4-byte elements wholly
+    // outside the partition: the word every one of its elements clamps to
+    __device__ __forceinline__ uint64_t edge4(uint64_t a) const { return a < base ? base : base + size - 4; }
 };
 
-// Check-mode hoisting: true iff every byte of [a, a+len) lies in the
+// A 16-byte-aligned vector at a holding four logical 4-byte accesses
+// (a, a+4, a+8, a+12).  Every mode but CLAMP fences it as one 16-byte access:
+// with base and size multiples of 16 the vector is wholly inside or wholly
+// outside the partition, and the mask / modulo fence of a+4k is F16(a)+4k.
+// CLAMP sends all four elements of an outside vector to one edge word, so the
+// vector is that word four times (a store keeps the last element, element
+// order).  Counted 4 per vector.  LD16 / LD4 / ST16 / ST4 are the cache
+// operators of the call site.
+template <int MODE, typename LD16, typename LD4>
+__device__ __forceinline__ uint4 vld4(const Fence<MODE, 16> &f, uint64_t a, uint32_t &nv, LD16 ld16, LD4 ld4) {
+    if constexpr (MODE == kClamp) {
+        if (f.inside(a)) return ld16(a);
+        nv += 4;
+        const uint32_t w = ld4(f.edge4(a));
+        return make_uint4(w, w, w, w);
+    } else {
+        if (f.go(a, nv, 4)) return ld16(f.addr(a));
+        return make_uint4(0, 0, 0, 0);
+    }
+}
+
+template <int MODE, typename ST16, typename ST4>
+__device__ __forceinline__ void vst4(const Fence<MODE, 16> &f, uint64_t a, uint4 v, uint32_t &nv, ST16 st16,
+                                     ST4 st4) {
+    if constexpr (MODE == kClamp) {
+        if (f.inside(a)) {
+            st16(a, v);
+        } else {
+            nv += 4;
+            st4(f.edge4(a), v.w);
+        }
+    } else {
+        if (f.go(a, nv, 4)) st16(f.addr(a), v);
+    }
+}
+
+// Hoisting (R-hoist): true iff every byte of [a, a+len) lies in the
 // partition (no 64-bit wraparound).  A CTA whose whole tile passes this test
 // performs exactly the accesses the per-access check would allow (all of
-// them) and refuses none, so it may run the unchecked body; only tiles that
-// touch or cross the partition edge pay for per-access checks.
+// them), refuses and counts none, and every modulo / clamp / mask fence of it
+// is the identity, so it may run the unfenced body; only tiles that touch or
+// cross the partition edge pay for per-access fencing.
 __device__ __forceinline__ bool range_in(const FenceDesc &fd, uint64_t a, uint64_t len) {
     const uint64_t off = a - fd.base;
     return !(fd.flags & kNoHoist) && len <= fd.size && off <= fd.size - len;

@@ -4,7 +4,13 @@
 
 namespace gd {
 
-enum Mode : int { kNone = 0, kMask = 1, kCheck = 2, kModulo = 3 };
+enum Mode : int { kNone = 0, kMask = 1, kCheck = 2, kModulo = 3, kMaskCount = 4, kClamp = 5 };
+
+// modes that count accesses outside the partition (the trusted counter)
+constexpr bool counts(int m) { return m == kCheck || m == kMaskCount || m == kClamp; }
+// modes whose fence is the identity, with nothing counted, for every access
+// inside the partition: a tile wholly inside may run the unfenced body (R-hoist)
+constexpr bool hoistable(int m) { return m == kCheck || m == kModulo || m == kMaskCount || m == kClamp; }
 
 // Launch-time partition descriptor.  Built on the host
 // from an immutable snapshot of the bounds-table row.

@@ -514,10 +514,12 @@ uint64_t desc_rows(int mode, uint64_t base, uint64_t size, uint64_t p, uint64_t 
     *pf = p;
     if (mode == kNone) return rows;
     uint64_t f;
-    if (mode == kMask) {
+    if (mode == kMask || mode == kMaskCount) {
         f = (p & ((size - 1) & ~15ull)) | base;
     } else if (mode == kModulo) {
         f = base + (((p - base) % size) & ~15ull);
+    } else if (mode == kClamp) {                        // largest legal 16-byte address <= p
+        f = p < base ? base : (p - base > size - 16 ? base + size - 16 : p & ~15ull);
     } else {
         if (p - base > size - 16 || (p & 15)) return 0;   // not a legal 16-byte access of the partition
         f = p;
@@ -568,8 +570,13 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
     uint64_t rA = desc_rows(w.mode, base, size, w.ptr[1], M, 2ull * K, 2ull * lda, &Af);
     uint64_t rB = desc_rows(w.mode, base, size, w.ptr[2], N, 2ull * K, 2ull * ldb, &Bf);
     const uint64_t rC = desc_rows(w.mode, base, size, w.ptr[0], M, 2ull * N, 2ull * ldc, &Cf);
-    if (w.mode == kCheck) {
-        const unsigned long long nv = (M - rA) + (N - rB) + (M - rC);
+    if (counts((int)w.mode)) {
+        // counted as check mode would refuse them: rows of each operand not
+        // wholly inside the partition at their unfenced address
+        uint64_t t;
+        const unsigned long long nv = (M - desc_rows(kCheck, base, size, w.ptr[1], M, 2ull * K, 2ull * lda, &t)) +
+                                      (N - desc_rows(kCheck, base, size, w.ptr[2], N, 2ull * K, 2ull * ldb, &t)) +
+                                      (M - desc_rows(kCheck, base, size, w.ptr[0], M, 2ull * N, 2ull * ldc, &t));
         if (nv) {
             k_add_violations<<<1, 1, 0, s>>>(a->d_stats + (uint64_t)w.tenant * GD_NUM_KINDS + GD_KIND_GEMM, nv);
             cudaError_t e = cudaGetLastError();

@@ -25,10 +25,12 @@ constexpr int kThreads = 256;
 constexpr int kU = 4;
 constexpr uint64_t kChunk = (uint64_t)kThreads * kU;   // index vectors per CTA
 
-__device__ __forceinline__ int4 ld_idx(uint64_t a) { return __ldcs(reinterpret_cast<const int4 *>(a)); }
 __device__ __forceinline__ uint4 ld_u4(uint64_t a) { return __ldcs(reinterpret_cast<const uint4 *>(a)); }
+__device__ __forceinline__ uint32_t ld_w(uint64_t a) { return __ldcs(reinterpret_cast<const unsigned int *>(a)); }
 __device__ __forceinline__ uint32_t ld_tab(uint64_t a) { return __ldcg(reinterpret_cast<const uint32_t *>(a)); }
+__device__ __forceinline__ uint4 ld_row(uint64_t a) { return __ldcg(reinterpret_cast<const uint4 *>(a)); }
 __device__ __forceinline__ void st_out(uint64_t a, uint4 v) { __stcs(reinterpret_cast<uint4 *>(a), v); }
+__device__ __forceinline__ void st_w(uint64_t a, uint32_t v) { __stcs(reinterpret_cast<unsigned int *>(a), v); }
 
 __device__ __forceinline__ uint64_t row_addr(uint64_t table, int32_t j) {
     return table + (uint64_t)((int64_t)j * 4);        // sext, scale in 64 bits
@@ -37,8 +39,7 @@ __device__ __forceinline__ uint64_t row_addr(uint64_t table, int32_t j) {
 template <int MODE>
 __device__ __forceinline__ uint32_t fenced_tab(const Fence<MODE, 4> &f4, uint64_t table, int32_t j, uint32_t &nv) {
     const uint64_t a = row_addr(table, j);
-    if (f4.ok(a)) return ld_tab(f4.addr(a));
-    nv++;
+    if (f4.go(a, nv, 1)) return ld_tab(f4.addr(a));
     return 0u;
 }
 
@@ -55,35 +56,27 @@ __device__ __forceinline__ void gather_chunk(const FenceDesc &fd, uint64_t out, 
                                              uint64_t v0, uint64_t nvec, uint32_t &nv) {
     const Fence<SMODE, 16> f16(fd);
     const Fence<TMODE, 4> f4(fd);
-    int4 j[kU];
+    uint4 j[kU];
 #pragma unroll
     for (int u = 0; u < kU; u++) {
         const uint64_t v = v0 + u * kThreads;
-        j[u] = make_int4(0, 0, 0, 0);
-        if (v < nvec) {
-            const uint64_t a = idx + 16 * v;
-            if (f16.ok(a)) j[u] = ld_idx(f16.addr(a));
-            else nv += 4;
-        }
+        j[u] = make_uint4(0, 0, 0, 0);
+        if (v < nvec) j[u] = vld4(f16, idx + 16 * v, nv, ld_u4, ld_w);
     }
     uint4 r[kU];
 #pragma unroll
     for (int u = 0; u < kU; u++) {
         if (v0 + u * kThreads < nvec) {
-            r[u].x = fenced_tab<TMODE>(f4, table, j[u].x, nv);
-            r[u].y = fenced_tab<TMODE>(f4, table, j[u].y, nv);
-            r[u].z = fenced_tab<TMODE>(f4, table, j[u].z, nv);
-            r[u].w = fenced_tab<TMODE>(f4, table, j[u].w, nv);
+            r[u].x = fenced_tab<TMODE>(f4, table, (int32_t)j[u].x, nv);
+            r[u].y = fenced_tab<TMODE>(f4, table, (int32_t)j[u].y, nv);
+            r[u].z = fenced_tab<TMODE>(f4, table, (int32_t)j[u].z, nv);
+            r[u].w = fenced_tab<TMODE>(f4, table, (int32_t)j[u].w, nv);
         }
     }
 #pragma unroll
     for (int u = 0; u < kU; u++) {
         const uint64_t v = v0 + u * kThreads;
-        if (v < nvec) {
-            const uint64_t a = out + 16 * v;
-            if (f16.ok(a)) st_out(f16.addr(a), r[u]);
-            else nv += 4;
-        }
+        if (v < nvec) vst4(f16, out + 16 * v, r[u], nv, st_out, st_w);
     }
 }
 
@@ -92,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) k_gather1(const __grid_constant__ Fe
                                                       uint64_t table, uint64_t idx, uint64_t nvec, uint32_t tail) {
     uint32_t nv = 0;
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, v0 = c0 + threadIdx.x;
-    if constexpr (MODE == kCheck || MODE == kModulo) {   // streams hoisted; random table accesses fenced
+    if constexpr (hoistable(MODE)) {     // streams hoisted; random table accesses fenced
         const uint64_t cn = chunk_len(nvec, c0);
         if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, out + 16 * c0, 16 * cn))
             gather_chunk<kNone, MODE>(fd, out, table, idx, v0, nvec, nv);
@@ -105,13 +98,11 @@ __global__ void __launch_bounds__(kThreads) k_gather1(const __grid_constant__ Fe
         const Fence<MODE, 4> f4(fd);
         const uint64_t ai = idx + 16 * nvec + 4 * threadIdx.x, ao = out + 16 * nvec + 4 * threadIdx.x;
         int32_t j = 0;
-        if (f4.ok(ai)) j = *reinterpret_cast<const int32_t *>(f4.addr(ai));
-        else nv++;
+        if (f4.go(ai, nv, 1)) j = *reinterpret_cast<const int32_t *>(f4.addr(ai));
         const uint32_t r = fenced_tab<MODE>(f4, table, j, nv);
-        if (f4.ok(ao)) *reinterpret_cast<uint32_t *>(f4.addr(ao)) = r;
-        else nv++;
+        if (f4.go(ao, nv, 1)) *reinterpret_cast<uint32_t *>(f4.addr(ao)) = r;
     }
-    if constexpr (MODE == kCheck) flush_violations(nv, fd.viol);
+    if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }
 
 // ---------------------------------------------------------------------------
@@ -128,22 +119,19 @@ __global__ void __launch_bounds__(kThreads) k_gatherD(const __grid_constant__ Fe
         int32_t j = 0;
         if (lane == 0) {
             const uint64_t ai = idx + 4 * i;
-            if (f4.ok(ai)) j = *reinterpret_cast<const int32_t *>(f4.addr(ai));
-            else nv++;
+            if (f4.go(ai, nv, 1)) j = *reinterpret_cast<const int32_t *>(f4.addr(ai));
         }
         j = __shfl_sync(0xffffffffu, j, 0);
         for (uint32_t d = lane; d < D; d += 32) {
             const uint64_t e = (uint64_t)((int64_t)j * (int64_t)D + (int64_t)d);
             const uint64_t at = table + e * 4;
             uint32_t r = 0;
-            if (f4.ok(at)) r = ld_tab(f4.addr(at));
-            else nv++;
+            if (f4.go(at, nv, 1)) r = ld_tab(f4.addr(at));
             const uint64_t ao = out + 4 * (i * D + d);
-            if (f4.ok(ao)) *reinterpret_cast<uint32_t *>(f4.addr(ao)) = r;
-            else nv++;
+            if (f4.go(ao, nv, 1)) *reinterpret_cast<uint32_t *>(f4.addr(ao)) = r;
         }
     }
-    if constexpr (MODE == kCheck) flush_violations(nv, fd.viol);
+    if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }
 
 // ---------------------------------------------------------------------------
@@ -202,21 +190,27 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
         const uint64_t i = row_of<P2>(sl, tpr, dv);
         const uint64_t t = sl - i * tpr;
         const uint64_t ai = idx + 4 * i;
-        const bool oki = live[k] && fi.ok_aligned(ai);
+        uint32_t ci = 0;
+        const bool oki = fi.go_aligned(ai, ci, 1) && live[k];        // ALU only: no branch
         j[k] = 0;
         if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fi.addr(ai)));
-        if (live[k] && !oki) nv += (t == 0);
+        if (live[k] && t == 0) nv += ci;                             // one index access per row
         ov[k] = out + 16 * (i * vpr + t);
         tv[k] = 16 * t;
     }
+    // (clamp: a warp-synchronising point after the index loads keeps ptxas
+    // from consuming each loaded index before the next load issues)
+    if constexpr (TMODE == kClamp) __syncwarp();
     uint64_t at[S][G];
     bool ok[S][G];
+    uint32_t cnt[S];
 #pragma unroll
     for (int k = 0; k < S; k++) {                       // 2. fenced table addresses (ALU only)
         const uint64_t rt = table + (uint64_t)((int64_t)j[k] * (int64_t)rowbytes) + tv[k];   // vector g = 0
         bool whole = false;                             // every vector of the slot in / unwrapped
         uint64_t fr = rt;
-        if constexpr (G > 1 && TMODE == kCheck) {
+        cnt[k] = 0;
+        if constexpr (G > 1 && (TMODE == kCheck || TMODE == kMaskCount || TMODE == kClamp)) {
             whole = range_in(fd, rt, 16 * tpr * (G - 1) + 16);
         } else if constexpr (G > 1 && TMODE == kModulo) {
             fr = ft.addr(rt);                           // rt is 16-aligned: fr - base = (rt - base) mod size
@@ -232,9 +226,15 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
             } else if (whole) {
                 at[k][g] = fr + 16 * tpr * g;
                 ok[k][g] = true;
+            } else if constexpr (TMODE == kClamp) {
+                // as check here (an outside vector is not loaded); step 3b
+                // then gives it its edge word four times
+                at[k][g] = a;
+                ok[k][g] = (a - fd.base) <= fd.size - 16;
+                cnt[k] += ok[k][g] ? 0u : 4u;
             } else {
                 at[k][g] = ft.addr(a);
-                ok[k][g] = ft.ok_aligned(a);
+                ok[k][g] = ft.go_aligned(a, cnt[k], 4);
             }
         }
     }
@@ -244,8 +244,20 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
 #pragma unroll
         for (int g = 0; g < G; g++) {
             r[k][g] = make_uint4(0, 0, 0, 0);
-            if (live[k] && ok[k][g]) r[k][g] = __ldcg(reinterpret_cast<const uint4 *>(at[k][g]));
-            if (live[k] && !ok[k][g]) nv += 4;
+            if (live[k] && ok[k][g]) r[k][g] = ld_row(at[k][g]);
+        }
+        if (live[k]) nv += cnt[k];
+    }
+    if constexpr (TMODE == kClamp) {                    // 3b. rare: outside vectors, after every load issued
+#pragma unroll
+        for (int k = 0; k < S; k++) {
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                if (live[k] && !ok[k][g]) {
+                    const uint32_t w = ld_tab(ft.edge4(at[k][g]));
+                    r[k][g] = make_uint4(w, w, w, w);
+                }
+            }
         }
     }
 #pragma unroll
@@ -253,22 +265,23 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
         if (live[k]) {
 #pragma unroll
             for (int g = 0; g < G; g++) {
-                const uint64_t ao = ov[k] + 16 * tpr * g;
-                if (fo.ok_aligned(ao)) st_out(fo.addr(ao), r[k][g]);
-                else nv += 4;
+                vst4(fo, ov[k] + 16 * tpr * g, r[k][g], nv, st_out, st_w);
             }
         }
     }
 }
 
+// 6 CTAs (48 warps) per SM: the row gather is bound by loads in flight, and
+// 5 CTAs measured 27-41 % slower at D = 32 / 64; clamp with G = 4 needs the
+// registers of 5 (no spill) and loses nothing there (D = 128).
 template <int MODE, int G, bool P2>
-__global__ void __launch_bounds__(kThreads, 6) k_gatherR(const __grid_constant__ FenceDesc fd, uint64_t out,
+__global__ void __launch_bounds__(kThreads, (MODE == kClamp && G == 4) ? 5 : 6) k_gatherR(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                       uint64_t table, uint64_t idx, uint64_t nslots, uint32_t tpr,
                                                       uint64_t dv) {
     constexpr uint64_t ch = (uint64_t)kThreads * (4 / G);
     uint32_t nv = 0;
     const uint64_t c0 = (uint64_t)blockIdx.x * ch, s0 = c0 + threadIdx.x;
-    if constexpr (MODE == kCheck || MODE == kModulo) {   // streams hoisted per CTA; table rows per slot
+    if constexpr (hoistable(MODE)) {     // streams hoisted per CTA; table rows per slot
         const uint64_t cn = nslots > c0 ? (nslots - c0 < ch ? nslots - c0 : ch) : 0;
         const uint64_t r0 = row_of<P2>(c0, tpr, dv);                   // rows this CTA touches
         const uint64_t nr = cn ? row_of<P2>(c0 + cn - 1, tpr, dv) - r0 + 1 : 0;
@@ -280,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_gatherR(const __grid_constant__
     } else {
         gatherr_chunk<MODE, MODE, G, P2>(fd, out, table, idx, s0, nslots, tpr, dv, nv);
     }
-    if constexpr (MODE == kCheck) flush_violations(nv, fd.viol);
+    if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }
 
 // ---------------------------------------------------------------------------
@@ -288,41 +301,76 @@ __global__ void __launch_bounds__(kThreads, 6) k_gatherR(const __grid_constant__
 // fenced access (atomics instrumented like stores) issued as a
 // no-return RED.E.ADD.
 // ---------------------------------------------------------------------------
+// CLAMP: every clamped RMW lands on one of the two edge words.  The thread
+// adds them up (u32 addition is associative and commutative, so the final
+// words are the same) and the CTA issues one atomic per edge (edge_flush).
+struct EdgeSums {
+    uint32_t lo = 0, hi = 0;
+    bool alo = false, ahi = false;
+};
+
 template <int MODE>
 __device__ __forceinline__ void fenced_red(const Fence<MODE, 4> &f4, uint64_t table, int32_t j, uint32_t v,
-                                           uint32_t &nv) {
+                                           uint32_t &nv, EdgeSums &es) {
     const uint64_t a = row_addr(table, j);
-    if (f4.ok(a)) atomicAdd(reinterpret_cast<unsigned int *>(f4.addr(a)), v);
-    else nv++;
+    if constexpr (MODE == kClamp) {
+        if (f4.inside(a)) {
+            atomicAdd(reinterpret_cast<unsigned int *>(a), v);
+        } else {
+            nv++;
+            if (a < f4.base) {
+                es.lo += v;
+                es.alo = true;
+            } else {
+                es.hi += v;
+                es.ahi = true;
+            }
+        }
+    } else {
+        if (f4.go(a, nv, 1)) atomicAdd(reinterpret_cast<unsigned int *>(f4.addr(a)), v);
+    }
+}
+
+// CTA-wide sums of the clamped RMWs, one atomic per edge word.  All threads.
+__device__ __forceinline__ void edge_flush(const FenceDesc &fd, const EdgeSums &es) {
+    __shared__ uint32_t sum[2], any[2];
+    if (threadIdx.x < 2) sum[threadIdx.x] = any[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t lo = __reduce_add_sync(0xffffffffu, es.lo), hi = __reduce_add_sync(0xffffffffu, es.hi);
+    const bool alo = __any_sync(0xffffffffu, es.alo), ahi = __any_sync(0xffffffffu, es.ahi);
+    if ((threadIdx.x & 31u) == 0) {
+        if (alo) { atomicAdd(&sum[0], lo); any[0] = 1; }
+        if (ahi) { atomicAdd(&sum[1], hi); any[1] = 1; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && any[0]) atomicAdd(reinterpret_cast<unsigned int *>(fd.base), sum[0]);
+    if (threadIdx.x == 1 && any[1]) atomicAdd(reinterpret_cast<unsigned int *>(fd.base + fd.size - 4), sum[1]);
 }
 
 template <int SMODE, int TMODE>
 __device__ __forceinline__ void scatter_chunk(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src,
-                                              uint64_t v0, uint64_t nvec, uint32_t &nv) {
+                                              uint64_t v0, uint64_t nvec, uint32_t &nv, EdgeSums &es) {
     const Fence<SMODE, 16> f16(fd);
     const Fence<TMODE, 4> f4(fd);
-    int4 j[kU];
+    uint4 j[kU];
     uint4 s[kU];
 #pragma unroll
     for (int u = 0; u < kU; u++) {
         const uint64_t v = v0 + u * kThreads;
-        j[u] = make_int4(0, 0, 0, 0);
+        j[u] = make_uint4(0, 0, 0, 0);
         s[u] = make_uint4(0, 0, 0, 0);
         if (v < nvec) {
-            const uint64_t ai = idx + 16 * v, as = src + 16 * v;
-            if (f16.ok(ai)) j[u] = ld_idx(f16.addr(ai));
-            else nv += 4;
-            if (f16.ok(as)) s[u] = ld_u4(f16.addr(as));
-            else nv += 4;
+            j[u] = vld4(f16, idx + 16 * v, nv, ld_u4, ld_w);
+            s[u] = vld4(f16, src + 16 * v, nv, ld_u4, ld_w);
         }
     }
 #pragma unroll
     for (int u = 0; u < kU; u++) {
         if (v0 + u * kThreads < nvec) {
-            fenced_red<TMODE>(f4, table, j[u].x, s[u].x, nv);
-            fenced_red<TMODE>(f4, table, j[u].y, s[u].y, nv);
-            fenced_red<TMODE>(f4, table, j[u].z, s[u].z, nv);
-            fenced_red<TMODE>(f4, table, j[u].w, s[u].w, nv);
+            fenced_red<TMODE>(f4, table, (int32_t)j[u].x, s[u].x, nv, es);
+            fenced_red<TMODE>(f4, table, (int32_t)j[u].y, s[u].y, nv, es);
+            fenced_red<TMODE>(f4, table, (int32_t)j[u].z, s[u].z, nv, es);
+            fenced_red<TMODE>(f4, table, (int32_t)j[u].w, s[u].w, nv, es);
         }
     }
 }
@@ -331,28 +379,28 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ FenceDesc fd, uint64_t table,
                                                       uint64_t idx, uint64_t src, uint64_t nvec, uint32_t tail) {
     uint32_t nv = 0;
+    EdgeSums es;
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, v0 = c0 + threadIdx.x;
-    if constexpr (MODE == kCheck || MODE == kModulo) {   // streams hoisted; random RMWs fenced
+    if constexpr (hoistable(MODE)) {     // streams hoisted; random RMWs fenced
         const uint64_t cn = chunk_len(nvec, c0);
         if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, src + 16 * c0, 16 * cn))
-            scatter_chunk<kNone, MODE>(fd, table, idx, src, v0, nvec, nv);
+            scatter_chunk<kNone, MODE>(fd, table, idx, src, v0, nvec, nv, es);
         else
-            scatter_chunk<MODE, MODE>(fd, table, idx, src, v0, nvec, nv);
+            scatter_chunk<MODE, MODE>(fd, table, idx, src, v0, nvec, nv, es);
     } else {
-        scatter_chunk<MODE, MODE>(fd, table, idx, src, v0, nvec, nv);
+        scatter_chunk<MODE, MODE>(fd, table, idx, src, v0, nvec, nv, es);
     }
     if (blockIdx.x == 0 && threadIdx.x < tail) {
         const Fence<MODE, 4> f4(fd);
         const uint64_t ai = idx + 16 * nvec + 4 * threadIdx.x, as = src + 16 * nvec + 4 * threadIdx.x;
         int32_t j = 0;
         uint32_t s = 0;
-        if (f4.ok(ai)) j = *reinterpret_cast<const int32_t *>(f4.addr(ai));
-        else nv++;
-        if (f4.ok(as)) s = *reinterpret_cast<const uint32_t *>(f4.addr(as));
-        else nv++;
-        fenced_red<MODE>(f4, table, j, s, nv);
+        if (f4.go(ai, nv, 1)) j = *reinterpret_cast<const int32_t *>(f4.addr(ai));
+        if (f4.go(as, nv, 1)) s = *reinterpret_cast<const uint32_t *>(f4.addr(as));
+        fenced_red<MODE>(f4, table, j, s, nv, es);
     }
-    if constexpr (MODE == kCheck) flush_violations(nv, fd.viol);
+    if constexpr (MODE == kClamp) edge_flush(fd, es);
+    if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }
 
 template <typename K>
@@ -414,6 +462,8 @@ cudaError_t launch_gather(int mode, const FenceDesc &fd, uint64_t out, uint64_t 
         case kNone: return gather_t<kNone>(fd, out, table, idx, n, D, s, g);
         case kMask: return gather_t<kMask>(fd, out, table, idx, n, D, s, g);
         case kModulo: return gather_t<kModulo>(fd, out, table, idx, n, D, s, g);
+        case kMaskCount: return gather_t<kMaskCount>(fd, out, table, idx, n, D, s, g);
+        case kClamp: return gather_t<kClamp>(fd, out, table, idx, n, D, s, g);
         default: return gather_t<kCheck>(fd, out, table, idx, n, D, s, g);
     }
 }
@@ -424,6 +474,8 @@ cudaError_t launch_scatter(int mode, const FenceDesc &fd, uint64_t table, uint64
         case kNone: return scatter_t<kNone>(fd, table, idx, src, n, s);
         case kMask: return scatter_t<kMask>(fd, table, idx, src, n, s);
         case kModulo: return scatter_t<kModulo>(fd, table, idx, src, n, s);
+        case kMaskCount: return scatter_t<kMaskCount>(fd, table, idx, src, n, s);
+        case kClamp: return scatter_t<kClamp>(fd, table, idx, src, n, s);
         default: return scatter_t<kCheck>(fd, table, idx, src, n, s);
     }
 }

@@ -25,6 +25,9 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kRows = 64;     // rows per CTA strip (a multiple of the rows loaded per step)
 
+__device__ __forceinline__ void st_v(uint64_t a, uint4 v) { __stcs(reinterpret_cast<uint4 *>(a), v); }
+__device__ __forceinline__ void st_w(uint64_t a, uint32_t v) { __stcs(reinterpret_cast<unsigned int *>(a), v); }
+
 template <int MODE, int kG>
 __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t W, uint64_t pitch,
                                       float c0, float c1, uint64_t c, uint64_t r0, uint64_t r1, uint32_t &nv) {
@@ -45,15 +48,23 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         ni += interior[k];
         nCv += interior[k] * (1u + (k >= 1) + (k <= 2));
     }
+    // ok = the vector's / word's accesses are not counted (check: performed);
+    // a clamped outside vector is its edge word four times (fence.cuh vld4)
     auto ldv = [&](uint64_t r, bool &ok) {
         const uint64_t a = in + 4 * (r * pitch + c);
-        ok = f16.ok(a);
-        return ok ? __ldg(reinterpret_cast<const float4 *>(f16.addr(a))) : make_float4(0.f, 0.f, 0.f, 0.f);
+        ok = counts(MODE) ? f16.inside(a) : true;
+        if constexpr (MODE == kClamp) {
+            if (ok) return __ldg(reinterpret_cast<const float4 *>(a));
+            const float w = __ldg(reinterpret_cast<const float *>(f16.edge4(a)));
+            return make_float4(w, w, w, w);
+        } else {
+            return f16.ok(a) ? __ldg(reinterpret_cast<const float4 *>(f16.addr(a))) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     };
     auto lds = [&](uint64_t e, bool &ok) {
         const uint64_t a = in + 4 * e;
-        ok = f4.ok(a);
-        return ok ? __ldg(reinterpret_cast<const float *>(f4.addr(a))) : 0.f;
+        ok = counts(MODE) ? f4.inside(a) : true;
+        return f4.ok(a) ? __ldg(reinterpret_cast<const float *>(f4.addr(a))) : 0.f;
     };
     bool okP, okC;
     float4 P = ldv(r0 - 1, okP);
@@ -96,7 +107,7 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
                     const float s = __fadd_rn(ns, we);
                     o[k] = __fmaf_rn(c1, s, __fmul_rn(c0, cc[k]));
                 }
-                if constexpr (MODE == kCheck) {
+                if constexpr (counts(MODE)) {
                     // per interior point: N, S, C loads; W from the own vector
                     // unless k == 0; E from the own vector unless k == 3
                     nv += ni * ((uint32_t)!okN + (uint32_t)!okS[g]) + nCv * (uint32_t)!okCC +
@@ -104,16 +115,16 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
                 }
                 const uint64_t ao = out + 4 * (rr * pitch + c);
                 if (all4) {
-                    if (f16.ok(ao))
-                        __stcs(reinterpret_cast<float4 *>(f16.addr(ao)), make_float4(o[0], o[1], o[2], o[3]));
-                    else nv += 4;
+                    vst4(f16, ao,
+                         make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
+                                    __float_as_uint(o[3])),
+                         nv, st_v, st_w);
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
                         if (!interior[k]) continue;
                         const uint64_t a = ao + 4 * k;
-                        if (f4.ok(a)) *reinterpret_cast<float *>(f4.addr(a)) = o[k];
-                        else nv++;
+                        if (f4.go(a, nv, 1)) *reinterpret_cast<float *>(f4.addr(a)) = o[k];
                     }
                 }
             }
@@ -145,9 +156,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__
     const uint64_t r0 = 1ull + (uint64_t)blockIdx.y * rows;
     const uint64_t r1 = (r0 + rows < (uint64_t)H - 1) ? r0 + rows : (uint64_t)H - 1;
     if (c < W && r0 < r1) {
-        if constexpr (MODE == kCheck || MODE == kModulo) {
+        if constexpr (hoistable(MODE)) {
             // conservative extents of everything this strip touches; inside the
-            // partition both the check and the modulo fence are the identity
+            // partition the fence is the identity and nothing is counted
             const uint64_t lo_in = in + 4 * ((r0 - 1) * pitch + c) - (c ? 4 : 0);
             const uint64_t hi_in = in + 4 * (r1 * pitch + c + 5);
             const uint64_t lo_out = out + 4 * (r0 * pitch + c), hi_out = out + 4 * ((r1 - 1) * pitch + c + 4);
@@ -160,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__
             strip<MODE, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
         }
     }
-    if constexpr (MODE == kCheck) flush_violations(nv, fd.viol);
+    if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }
 
 template <int MODE>
@@ -187,6 +198,8 @@ cudaError_t launch_stencil(int mode, const FenceDesc &fd, uint64_t out, uint64_t
         case kNone: return stencil_t<kNone>(fd, out, in, H, W, pitch, c0, c1, s, g.sms);
         case kMask: return stencil_t<kMask>(fd, out, in, H, W, pitch, c0, c1, s, g.sms);
         case kModulo: return stencil_t<kModulo>(fd, out, in, H, W, pitch, c0, c1, s, g.sms);
+        case kMaskCount: return stencil_t<kMaskCount>(fd, out, in, H, W, pitch, c0, c1, s, g.sms);
+        case kClamp: return stencil_t<kClamp>(fd, out, in, H, W, pitch, c0, c1, s, g.sms);
         default: return stencil_t<kCheck>(fd, out, in, H, W, pitch, c0, c1, s, g.sms);
     }
 }

@@ -8,9 +8,9 @@
 // this schedule against 5.9 TB/s for a persistent grid-stride loop.
 // Every 16-byte access address goes through the fence of MODE (fence.cuh);
 // the byte / element tail uses the fence at its own width.  The mask fence
-// is 2 LOP3 per 16 bytes; check mode hoists one range test per CTA chunk and
-// falls back to per-access checks only for chunks that touch the partition
-// edge (identical results: see range_in).
+// is 2 LOP3 per 16 bytes; the other fenced modes hoist one range test per CTA
+// chunk and fence per access only chunks that touch the partition edge
+// (identical results: see range_in).
 #include "fence.cuh"
 #include "kernels.h"
 
@@ -23,8 +23,8 @@ constexpr uint64_t kChunk = (uint64_t)kThreads * kU;   // vectors per CTA
 
 __device__ __forceinline__ uint4 ld16(uint64_t a) { return __ldcs(reinterpret_cast<const uint4 *>(a)); }
 __device__ __forceinline__ void st16(uint64_t a, uint4 v) { __stcs(reinterpret_cast<uint4 *>(a), v); }
-__device__ __forceinline__ float4 ld16f(uint64_t a) { return __ldcs(reinterpret_cast<const float4 *>(a)); }
-__device__ __forceinline__ void st16f(uint64_t a, float4 v) { __stcs(reinterpret_cast<float4 *>(a), v); }
+__device__ __forceinline__ uint32_t ld4(uint64_t a) { return __ldcs(reinterpret_cast<const unsigned int *>(a)); }
+__device__ __forceinline__ void st4(uint64_t a, uint32_t v) { __stcs(reinterpret_cast<unsigned int *>(a), v); }
 
 // ---------------------------------------------------------------------------
 // K1: dst[0:n) = src[0:n).  Logical accesses (oracle or_copy): per 16-byte
@@ -41,8 +41,7 @@ __device__ __forceinline__ void copy_chunk(const FenceDesc &fd, uint64_t dst, ui
         r[u] = make_uint4(0, 0, 0, 0);
         if (v < nvec) {
             const uint64_t a = src + 16 * v;
-            if (f.ok(a)) r[u] = ld16(f.addr(a));
-            else nv++;
+            if (f.go(a, nv, 1)) r[u] = ld16(f.addr(a));
         }
     }
 #pragma unroll
@@ -50,8 +49,7 @@ __device__ __forceinline__ void copy_chunk(const FenceDesc &fd, uint64_t dst, ui
         const uint64_t v = v0 + u * kThreads;
         if (v < nvec) {
             const uint64_t a = dst + 16 * v;
-            if (f.ok(a)) st16(f.addr(a), r[u]);
-            else nv++;
+            if (f.go(a, nv, 1)) st16(f.addr(a), r[u]);
         }
     }
 }
@@ -62,7 +60,7 @@ __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ Fence
     uint32_t nv = 0;
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
     const uint64_t v0 = c0 + threadIdx.x;
-    if constexpr (MODE == kCheck || MODE == kModulo) {   // both fences are the identity inside the partition
+    if constexpr (hoistable(MODE)) {     // the fence is the identity inside the partition
         const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
         if (cn && range_in(fd, src + 16 * c0, 16 * cn) && range_in(fd, dst + 16 * c0, 16 * cn))
             copy_chunk<kNone>(fd, dst, src, v0, nvec, nv);
@@ -75,47 +73,42 @@ __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ Fence
         const Fence<MODE, 1> f1(fd);
         const uint64_t as = src + 16 * nvec + threadIdx.x, ad = dst + 16 * nvec + threadIdx.x;
         uint8_t b = 0;
-        if (f1.ok(as)) b = *reinterpret_cast<const uint8_t *>(f1.addr(as));
-        else nv++;
-        if (f1.ok(ad)) *reinterpret_cast<uint8_t *>(f1.addr(ad)) = b;
-        else nv++;
+        if (f1.go(as, nv, 1)) b = *reinterpret_cast<const uint8_t *>(f1.addr(as));
+        if (f1.go(ad, nv, 1)) *reinterpret_cast<uint8_t *>(f1.addr(ad)) = b;
     }
-    if constexpr (MODE == kCheck) flush_violations(nv, fd.viol);
+    if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }
 
 // ---------------------------------------------------------------------------
 // K2: y[i] = fmaf(alpha, x[i], y[i]).  Logical accesses (or_saxpy): per
-// element load x, load y, store y -- a refused 16-byte vector is 4 refused
-// element accesses (a 16-byte-aligned vector of a >= 4 KiB pow2 partition is
-// either wholly inside or wholly outside it).
+// element load x, load y, store y -- a 16-byte vector is four element
+// accesses (vld4 / vst4).
 // ---------------------------------------------------------------------------
 template <int MODE>
 __device__ __forceinline__ void saxpy_chunk(const FenceDesc &fd, float alpha, uint64_t x, uint64_t y, uint64_t v0,
                                             uint64_t nvec, uint32_t &nv) {
     const Fence<MODE, 16> f(fd);
-    float4 xv[kU], yv[kU];
+    uint4 xv[kU], yv[kU];
 #pragma unroll
     for (int u = 0; u < kU; u++) {
         const uint64_t v = v0 + u * kThreads;
-        xv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        xv[u] = make_uint4(0, 0, 0, 0);
         yv[u] = xv[u];
         if (v < nvec) {
-            const uint64_t ax = x + 16 * v, ay = y + 16 * v;
-            if (f.ok(ax)) xv[u] = ld16f(f.addr(ax));
-            else nv += 4;
-            if (f.ok(ay)) yv[u] = ld16f(f.addr(ay));
-            else nv += 4;
+            xv[u] = vld4(f, x + 16 * v, nv, ld16, ld4);
+            yv[u] = vld4(f, y + 16 * v, nv, ld16, ld4);
         }
     }
 #pragma unroll
     for (int u = 0; u < kU; u++) {
         const uint64_t v = v0 + u * kThreads;
         if (v < nvec) {
-            const uint64_t ay = y + 16 * v;
-            const float4 r = make_float4(__fmaf_rn(alpha, xv[u].x, yv[u].x), __fmaf_rn(alpha, xv[u].y, yv[u].y),
-                                         __fmaf_rn(alpha, xv[u].z, yv[u].z), __fmaf_rn(alpha, xv[u].w, yv[u].w));
-            if (f.ok(ay)) st16f(f.addr(ay), r);
-            else nv += 4;
+            const uint4 r = make_uint4(
+                __float_as_uint(__fmaf_rn(alpha, __uint_as_float(xv[u].x), __uint_as_float(yv[u].x))),
+                __float_as_uint(__fmaf_rn(alpha, __uint_as_float(xv[u].y), __uint_as_float(yv[u].y))),
+                __float_as_uint(__fmaf_rn(alpha, __uint_as_float(xv[u].z), __uint_as_float(yv[u].z))),
+                __float_as_uint(__fmaf_rn(alpha, __uint_as_float(xv[u].w), __uint_as_float(yv[u].w))));
+            vst4(f, y + 16 * v, r, nv, st16, st4);
         }
     }
 }
@@ -126,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_saxpy(const __grid_constant__ Fenc
     uint32_t nv = 0;
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk;
     const uint64_t v0 = c0 + threadIdx.x;
-    if constexpr (MODE == kCheck || MODE == kModulo) {   // both fences are the identity inside the partition
+    if constexpr (hoistable(MODE)) {     // the fence is the identity inside the partition
         const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
         if (cn && range_in(fd, x + 16 * c0, 16 * cn) && range_in(fd, y + 16 * c0, 16 * cn))
             saxpy_chunk<kNone>(fd, alpha, x, y, v0, nvec, nv);
@@ -139,14 +132,11 @@ __global__ void __launch_bounds__(kThreads) k_saxpy(const __grid_constant__ Fenc
         const Fence<MODE, 4> f4(fd);
         const uint64_t ax = x + 16 * nvec + 4 * threadIdx.x, ay = y + 16 * nvec + 4 * threadIdx.x;
         float xs = 0.f, ys = 0.f;
-        if (f4.ok(ax)) xs = *reinterpret_cast<const float *>(f4.addr(ax));
-        else nv++;
-        if (f4.ok(ay)) ys = *reinterpret_cast<const float *>(f4.addr(ay));
-        else nv++;
-        if (f4.ok(ay)) *reinterpret_cast<float *>(f4.addr(ay)) = __fmaf_rn(alpha, xs, ys);
-        else nv++;
+        if (f4.go(ax, nv, 1)) xs = *reinterpret_cast<const float *>(f4.addr(ax));
+        if (f4.go(ay, nv, 1)) ys = *reinterpret_cast<const float *>(f4.addr(ay));
+        if (f4.go(ay, nv, 1)) *reinterpret_cast<float *>(f4.addr(ay)) = __fmaf_rn(alpha, xs, ys);
     }
-    if constexpr (MODE == kCheck) flush_violations(nv, fd.viol);
+    if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }
 
 // ---------------------------------------------------------------------------
@@ -198,6 +188,8 @@ cudaError_t launch_copy(int mode, const FenceDesc &fd, uint64_t dst, uint64_t sr
         case kNone: return copy_t<kNone>(fd, dst, src, nbytes, s);
         case kMask: return copy_t<kMask>(fd, dst, src, nbytes, s);
         case kModulo: return copy_t<kModulo>(fd, dst, src, nbytes, s);
+        case kMaskCount: return copy_t<kMaskCount>(fd, dst, src, nbytes, s);
+        case kClamp: return copy_t<kClamp>(fd, dst, src, nbytes, s);
         default: return copy_t<kCheck>(fd, dst, src, nbytes, s);
     }
 }
@@ -208,6 +200,8 @@ cudaError_t launch_saxpy(int mode, const FenceDesc &fd, float alpha, uint64_t x,
         case kNone: return saxpy_t<kNone>(fd, alpha, x, y, n, s);
         case kMask: return saxpy_t<kMask>(fd, alpha, x, y, n, s);
         case kModulo: return saxpy_t<kModulo>(fd, alpha, x, y, n, s);
+        case kMaskCount: return saxpy_t<kMaskCount>(fd, alpha, x, y, n, s);
+        case kClamp: return saxpy_t<kClamp>(fd, alpha, x, y, n, s);
         default: return saxpy_t<kCheck>(fd, alpha, x, y, n, s);
     }
 }

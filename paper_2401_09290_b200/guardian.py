@@ -23,8 +23,9 @@ STATUS = ["GD_OK", "GD_ERR_INVALID_ARG", "GD_ERR_NOT_POW2", "GD_ERR_DEVICE_OOM",
 (GD_ERR_INVALID_ARG, GD_ERR_NOT_POW2, GD_ERR_DEVICE_OOM, GD_ERR_PARTITION_OOM, GD_ERR_UNKNOWN_PARTITION,
  GD_ERR_UNKNOWN_ALLOC, GD_ERR_ALIGN, GD_ERR_OOB_RANGE, GD_ERR_UNSUPPORTED, GD_ERR_CUDA) = range(1, 11)
 GD_MODE_NONE, GD_MODE_MASK, GD_MODE_CHECK = 0, 1, 2
-GD_MODE_MODULO = 3
-MODES = {"none": GD_MODE_NONE, "mask": GD_MODE_MASK, "check": GD_MODE_CHECK, "modulo": GD_MODE_MODULO}
+GD_MODE_MODULO, GD_MODE_MASK_COUNT, GD_MODE_CLAMP = 3, 4, 5
+MODES = {"none": GD_MODE_NONE, "mask": GD_MODE_MASK, "check": GD_MODE_CHECK, "modulo": GD_MODE_MODULO,
+         "maskcount": GD_MODE_MASK_COUNT, "clamp": GD_MODE_CLAMP}
 GD_PART_POW2 = 1
 (GD_KIND_COPY, GD_KIND_SAXPY, GD_KIND_GATHER, GD_KIND_SCATTER, GD_KIND_STENCIL, GD_KIND_GEMM) = range(6)
 GD_NUM_KINDS = 6

@@ -111,7 +111,7 @@ def test_gemm_all_ones_exact(arenas):
     assert (_bf16_to_f32(got) == K).all()
 
 
-@pytest.mark.parametrize("mode", ["mask", "check"])
+@pytest.mark.parametrize("mode", ["mask", "check", "maskcount", "clamp"])
 def test_gemm_A_past_end_rows_are_zero(arenas, mode):
     """A placed so its last 64 rows lie past end: the
     descriptor clamp reads them as zero, so those C rows are exactly 0."""
@@ -123,12 +123,12 @@ def test_gemm_A_past_end_rows_are_zero(arenas, mode):
     upload(pa, synth.bf16_bits_uniform(rng, (M - 64) * K))
     upload(p.base, synth.bf16_bits_uniform(rng, N * K))
     pc = p.base + 4 * MiB
-    _run(a, p, mode, pa, p.base, pc, M, N, K, K, K, N, expect_viol=64 if mode == "check" else 0)
+    _run(a, p, mode, pa, p.base, pc, M, N, K, K, K, N, expect_viol=0 if mode == "mask" else 64)
     C = download(pc, 2 * M * N).view(np.uint16).reshape(M, N)
     assert (C[M - 64:] == 0).all()
 
 
-@pytest.mark.parametrize("mode", ["mask", "check"])
+@pytest.mark.parametrize("mode", ["mask", "check", "maskcount", "clamp"])
 def test_gemm_C_past_end_rows_not_stored(arenas, mode):
     a, parts = _setup(arenas)
     p = parts[1]
@@ -138,13 +138,14 @@ def test_gemm_C_past_end_rows_not_stored(arenas, mode):
     upload(p.base + 4 * MiB, synth.bf16_bits_uniform(rng, N * K))
     upload(p.base + 8 * MiB, synth.random_bytes(rng, 8 * MiB))
     pc = p.end - (M - 30) * N * 2                          # last 30 rows of C past end
-    _run(a, p, mode, p.base, p.base + 4 * MiB, pc, M, N, K, K, K, N, expect_viol=30 if mode == "check" else 0)
+    _run(a, p, mode, p.base, p.base + 4 * MiB, pc, M, N, K, K, K, N, expect_viol=0 if mode == "mask" else 30)
 
 
-@pytest.mark.parametrize("mode", ["mask", "check"])
+@pytest.mark.parametrize("mode", ["mask", "check", "maskcount", "clamp"])
 def test_gemm_operand_in_victim(arenas, mode):
     """B points into another tenant's partition: check reads no rows (C = 0),
-    mask fences the descriptor start into the own partition."""
+    mask fences the descriptor start into the own partition, clamp moves it
+    to the own base (the partition below is the victim)."""
     a, parts = _setup(arenas)
     p, victim = parts[1], parts[0]
     M, N, K = 128, 256, 128
@@ -152,7 +153,9 @@ def test_gemm_operand_in_victim(arenas, mode):
     upload(p.base, synth.bf16_bits_uniform(rng, M * K))
     upload(victim.base + 4 * MiB, synth.bf16_bits_uniform(rng, N * K))
     upload(p.base + 4 * MiB, synth.bf16_bits_uniform(rng, N * K))       # what the mask lands on
+    if mode == "clamp":
+        assert victim.base < p.base
     vb = download(victim.base, victim.size)
     _run(a, p, mode, p.base, victim.base + 4 * MiB, p.base + 8 * MiB, M, N, K, K, K, N,
-         expect_viol=N if mode == "check" else 0)
+         expect_viol=0 if mode == "mask" else N)
     assert np.array_equal(download(victim.base, victim.size), vb)

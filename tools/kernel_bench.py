@@ -39,11 +39,14 @@ def paper_mean(xs):
     return statistics.mean(core)
 
 
+MODES = ["none", "mask", "check", "modulo"]          # --modes
+
+
 def time_modes(launch, reps, warm=3, extra=None):
     """launch(mode, stream) -> None; interleaved none/mask/check (+ extra
     reference launches {name: fn(stream)} timed in the same rotation)."""
     s = torch.cuda.Stream()
-    res = {m: [] for m in ("none", "mask", "check", "modulo")}
+    res = {m: [] for m in MODES}
     extra = extra or {}
     res.update({k: [] for k in extra})
 
@@ -72,7 +75,7 @@ def time_modes_batched(launch, reps, batch=50, warm=3):
     """L2-resident regime: kernels of a few microseconds are timed as a batch
     of back-to-back launches between two events (per-launch mean)."""
     s = torch.cuda.Stream()
-    res = {m: [] for m in ("none", "mask", "check", "modulo")}
+    res = {m: [] for m in MODES}
     with torch.cuda.stream(s):
         for m in res:
             for _ in range(warm):
@@ -96,7 +99,7 @@ def summarize(name, res, work, unit, peak):
         rate = work / (med / 1e3) / (1e9 if unit == "GB/s" else 1e12)
         out[m] = {"ms_median": round(med, 4), "ms_paper_mean": round(paper_mean(xs), 4), unit: round(rate, 1),
                   "frac_of_peak": round(rate / peak, 4)}
-    for m in ("mask", "check", "modulo"):
+    for m in (m for m in MODES if m != "none"):
         out[m]["overhead_pct"] = round(100 * (out[m]["ms_median"] / out["none"]["ms_median"] - 1), 2)
     print(f"{name:28s} " + "  ".join(f"{m}: {out[m][unit]:8.1f} {unit}" + (f" ({out[m]['overhead_pct']:+.2f}%)"
                                                                            if m != 'none' else '')
@@ -108,7 +111,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=12)
     ap.add_argument("--only", default="")
+    ap.add_argument("--modes", default=",".join(MODES),
+                    help="fence modes timed interleaved (none first): none,mask,check,modulo,maskcount,clamp")
     args = ap.parse_args()
+    MODES[:] = args.modes.split(",")
+    assert MODES[0] == "none", "none (the unfenced twin) must come first"
     only = set(args.only.split(",")) if args.only else None
     hbm, bf16, bf16s = peaks()
     torch.cuda.set_device(0)

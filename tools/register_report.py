@@ -14,7 +14,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "paper_2401_09290_b200", "build")
-MODES = {"0": "none", "1": "mask", "2": "check", "3": "modulo"}
+MODES = {"0": "none", "1": "mask", "2": "check", "3": "modulo", "4": "maskcount", "5": "clamp"}
 
 
 def demangle(names):
