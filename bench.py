@@ -30,6 +30,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 GiB = 1 << 30
+# fence modes in gd_mode order; the unfenced twin first (overheads are against it)
+ALL_MODES = ("none", "mask", "check", "modulo", "maskcount", "clamp")
 TENANTS = 8
 PART = 1 << 34                    # 16 GiB
 ARENA = TENANTS * PART            # 2^37
@@ -292,7 +294,7 @@ class Workload:
         }
         s = self.streams[0]
         out = {}
-        modes = ("none", "mask", "check", "modulo")
+        modes = ALL_MODES
         for name, (fn, work, unit) in kern.items():
             times = {m: [] for m in modes}
             with torch.cuda.stream(s):
@@ -376,8 +378,8 @@ def run_gpu(args):
     ms_per_step = ms / args.steps
     value = world * STEP_BYTES_PER_GPU / (ms_per_step / 1e3) / 1e9
 
-    # ---- overhead vs the unfenced twin: interleaved None/Mask/Check/Modulo ----
-    modes = ("none", "mask", "check", "modulo")
+    # ---- overhead vs the unfenced twin: every mode, interleaved ----
+    modes = ALL_MODES
     per_mode = {m: [] for m in modes}
     for _ in range(args.reps):
         for m in modes:
@@ -394,7 +396,7 @@ def run_gpu(args):
             solo[(kind, m)] = (statistics.mean(d), nbytes)
     sx_ms, sx_bytes = solo[("saxpy", args.mode)]
     achieved = sx_bytes / (sx_ms / 1e3) / 1e9
-    mode_id = {"none": 0, "mask": 1, "check": 2, "modulo": 3}[args.mode]
+    mode_id = ALL_MODES.index(args.mode)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": ncu_traffic(f"k_saxpy<{mode_id}>"),
                 "kernel": f"k_saxpy<{args.mode}>", "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json)",
@@ -442,7 +444,7 @@ def run_gpu(args):
                 t = allreduce([row[m]["ms"]])[0]
                 row[m] = {"ms": round(t, 4), row[m]["unit"]: round(world * row[m]["work"] / (t / 1e3) /
                                                                     (1e9 if row[m]["unit"] == "GB/s" else 1e12), 1)}
-            for m in ("mask", "check", "modulo"):
+            for m in ALL_MODES[1:]:
                 row[m]["overhead_pct"] = round(100 * (row[m]["ms"] / row["none"]["ms"] - 1), 2)
 
     cpu = None
@@ -574,7 +576,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--mode", default="mask", choices=["none", "mask", "check", "modulo"])
+    ap.add_argument("--mode", default="mask", choices=list(ALL_MODES))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--reps", type=int, default=5, help="interleaved none/mask/check repetitions")
     ap.add_argument("--e2e-steps", type=int, default=2)
