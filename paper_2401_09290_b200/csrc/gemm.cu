@@ -53,7 +53,7 @@ constexpr uint32_t TMEM_COLS = ACC * BN;           // 512
 // raster group (m-blocks): probe (tools/gemm_group_probe.sh) at 8192^3 -- DRAM
 // reads 1.52 / 1.10 / 1.25 / 2.27 GB for groups 4 / 8 / 16 / 32, and under the
 // 1 kW power cap sustained TFLOP/s follow the DRAM traffic (8 is best)
-constexpr uint32_t GROUP_M = 8;
+constexpr uint32_t GROUP_M = 16;   // raster group (m-blocks); probe: profiles/r01_gemm_krev_probe.txt
 
 // instruction descriptor: D f32, A/B bf16, both K-major, N=256, M=128
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -337,7 +337,8 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-        const __grid_constant__ CUtensorMap tmC, uint32_t K, uint32_t tm, uint32_t tn, uint32_t group) {
+        const __grid_constant__ CUtensorMap tmC, uint32_t K, uint32_t tm, uint32_t tn, uint32_t group,
+        uint32_t krev) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *epi = smem + STAGES2 * STAGE2_BYTES;                  // C staging, 16 KB
@@ -377,12 +378,15 @@ k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer (both CTAs) ----------------
-        uint32_t it = 0;
+        uint32_t it = 0, tl = 0;
         bool alive = true;
-        for (uint32_t t = pair; t < ntiles && alive; t += npairs) {
+        for (uint32_t t = pair; t < ntiles && alive; t += npairs, tl++) {
             uint32_t mb, nb;
             tile_coords(t, tm, tn, group, mb, nb);
             const int row_a = (int)(mb * 2 * BM + rank * BM), row_b = (int)(nb * BN + rank * B_HALF);
+            // krev: odd waves walk K backwards, so a wave starts on the K slices
+            // the previous wave (same A panels) touched last -- still in L2
+            const bool back = krev && (tl & 1);
             for (uint32_t kb = 0; kb < nkb; kb++, it++) {
                 const uint32_t s = it % STAGES2, ph = (it / STAGES2) & 1;
                 if (!mbar_wait(smem_u32(&empty[s]), ph ^ 1)) { alive = false; break; }
@@ -394,7 +398,7 @@ k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtenso
                              "r"(STAGE2_BYTES)
                              : "memory");
                 const uint32_t sa = smem_u32(smem + s * STAGE2_BYTES), sb = sa + A_BYTES;
-                const int kc = (int)(kb * BK);
+                const int kc = (int)((back ? nkb - 1 - kb : kb) * BK);
                 asm volatile(
                     "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
                     " [%0], [%1, {%3, %4}], [%2];" ::"r"(sa), "l"(&tmA), "r"(fb), "r"(kc), "r"(row_a)
@@ -612,6 +616,10 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
         const int v = e ? atoi(e) : 0;
         return (uint32_t)(v > 0 ? v : GROUP_M);
     }();
+    static const uint32_t krev = [] {                  // K-direction alternation per wave (default on)
+        const char *e = getenv("GD_GEMM_KREV");
+        return (uint32_t)(e ? atoi(e) : 1);
+    }();
     if (rC >= 2 * BM && !force1 && g.sms >= 2) {
         // 2-SM path: B staged in N halves per CTA
         CUtensorMap tmB2;
@@ -620,7 +628,7 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
         const uint32_t tm = (uint32_t)((rC + 2 * BM - 1) / (2 * BM)), tn = (N + BN - 1) / BN;
         const uint32_t ntiles = tm * tn, pairs_max = (uint32_t)g.sms / 2;
         const uint32_t grid = 2 * (ntiles < pairs_max ? ntiles : pairs_max);
-        k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, tmC, K, tm, tn, group);
+        k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, tmC, K, tm, tn, group, krev);
         return cuda_status(cudaGetLastError());
     }
     if (!make_map(&tmB, Bf, K, rB, ldB, BN)) return GD_ERR_UNSUPPORTED;
