@@ -216,7 +216,7 @@ class Workload:
         else:
             self.arena.saxpy(p.id, mode, ALPHA, p.base + OFF_X, p.base + OFF_Y, SAXPY_N, stream=s)
 
-    def c5(self, launches=20, mode="check", seed_base=5000):
+    def c5(self, launches=20, mode="check", seed_base=5000, policy="round_robin"):
         """BASELINE.json configs[4] on this GPU: t0-t2 fenced copy (4 GiB),
         t3-t5 fenced gather (C3: 2^26 indices, 1 % planted OOB), t6-t7 fenced
         GEMM 8192^3, `launches` launches each, issued round-robin by the
@@ -258,7 +258,7 @@ class Workload:
         start.record(root)
         for s in self.streams:
             s.wait_event(start)
-        self.step(queue)
+        self.arena.launcher_run(queue, self.streams, policy=policy)
         for s in self.streams:
             e = torch.cuda.Event()
             e.record(s)
@@ -417,10 +417,19 @@ def run_gpu(args):
     c5 = None
     c5_expected = 0
     if not args.no_c5:
-        c5_ms, c5_bytes, c5_flops, c5_planted = w.c5(launches=args.c5_launches)
-        c5_ms_max = allreduce([c5_ms])[0]
+        # the paper's launcher (round robin, free-running tenant streams) and the
+        # interference-aware memory-lane policy (include/guardian.h gd_policy);
+        # the violation check below reads the counters of the last run
+        by_policy = {}
+        for pol in ("round_robin", "memory_lane"):
+            c5_ms, c5_bytes, c5_flops, c5_planted = w.c5(launches=args.c5_launches, policy=pol)
+            by_policy[pol] = allreduce([c5_ms])[0]
+        best = min(by_policy, key=by_policy.get)
+        c5_ms_max = by_policy[best]
         c5_expected = int(allreduce([float(c5_planted)], op="sum")[0])
-        c5 = {"makespan_ms": round(c5_ms_max, 3), "launches_per_tenant": args.c5_launches, "mode": "check",
+        c5 = {"makespan_ms": round(c5_ms_max, 3), "policy": best,
+              "makespan_ms_by_policy": {k: round(v, 3) for k, v in by_policy.items()},
+              "launches_per_tenant": args.c5_launches, "mode": "check",
               "memory_GBps": round(world * c5_bytes / (c5_ms_max / 1e3) / 1e9, 1),
               "gemm_TFLOPs": round(world * c5_flops / (c5_ms_max / 1e3) / 1e12, 1),
               "tenants": "t0-2 copy 4 GiB, t3-5 gather 2^26 (1% OOB), t6-7 GEMM 8192^3 bf16"}

@@ -261,6 +261,28 @@ gd_status gd_schedule_round_robin(const gd_work *items, uint32_t n_items, uint32
 gd_status gd_launcher_run(gd_arena *a, const gd_work *items, uint32_t n_items, void *const *streams,
                           uint32_t n_streams, uint32_t *order_out);
 
+/* Issue policies (gd_launcher_run_policy).
+ *  ROUND_ROBIN : gd_launcher_run, the paper's launcher:
+ *                every tenant's stream free-running, the hardware overlaps.
+ *  NO_TENSOR_RANDOM : the same order and streams, plus cross-stream event
+ *                waits so that a tensor-core kernel (GEMM) never runs
+ *                concurrently with a random-access kernel (gather, scatter):
+ *                each waits for every such kernel of the other class issued
+ *                before it.  Streaming kernels (copy, saxpy, stencil) stay
+ *                free.  Measured on B200 (tools/c5_policies.py): GEMM with a
+ *                concurrent gather is 22 % slower than the two serialised
+ *                (the gather's random DRAM traffic stalls the GEMM's TMA
+ *                pipeline), while GEMM with a copy is 13 % faster, and
+ *                copy / gather pairs are neutral.  Results are identical
+ *                (different tenants never share memory); only overlap changes.
+ *  MEMORY_LANE : NO_TENSOR_RANDOM, and the memory-bound kernels (all but
+ *                GEMM) run one after another in issue order on a single
+ *                "HBM lane" (event chain across the tenant streams), so only
+ *                tensor-core work overlaps them.                             */
+typedef enum { GD_POLICY_ROUND_ROBIN = 0, GD_POLICY_NO_TENSOR_RANDOM = 1, GD_POLICY_MEMORY_LANE = 2 } gd_policy;
+gd_status gd_launcher_run_policy(gd_arena *a, const gd_work *items, uint32_t n_items, void *const *streams,
+                                 uint32_t n_streams, uint32_t policy, uint32_t *order_out);
+
 /* ---- captured steps (CUDA graphs) ------------------------------------------ */
 typedef struct gd_graph gd_graph;     /* opaque, library-owned */
 /* Capture one gd_launcher_run of `items` over n_streams library-owned tenant

@@ -626,7 +626,13 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
         std::memset(&tmB2, 0, sizeof(tmB2));
         if (!make_map(&tmB2, Bf, K, rB, ldB, B_HALF)) return GD_ERR_UNSUPPORTED;
         const uint32_t tm = (uint32_t)((rC + 2 * BM - 1) / (2 * BM)), tn = (N + BN - 1) / BN;
-        const uint32_t ntiles = tm * tn, pairs_max = (uint32_t)g.sms / 2;
+        static const uint32_t sm_cap = [] {              // SMs a GEMM may hold (co-scheduling knob)
+            const char *e = getenv("GD_GEMM_MAX_SMS");
+            const int v = e ? atoi(e) : 0;
+            return (uint32_t)(v >= 2 ? v : 1u << 30);
+        }();
+        const uint32_t sms = (uint32_t)g.sms < sm_cap ? (uint32_t)g.sms : sm_cap;
+        const uint32_t ntiles = tm * tn, pairs_max = sms / 2;
         const uint32_t grid = 2 * (ntiles < pairs_max ? ntiles : pairs_max);
         k_gemm2<<<grid, THREADS, SMEM2_BYTES, s>>>(tmA, tmB2, tmC, K, tm, tn, group, krev);
         return cuda_status(cudaGetLastError());

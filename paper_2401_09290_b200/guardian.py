@@ -26,6 +26,9 @@ GD_MODE_NONE, GD_MODE_MASK, GD_MODE_CHECK = 0, 1, 2
 GD_MODE_MODULO, GD_MODE_MASK_COUNT, GD_MODE_CLAMP = 3, 4, 5
 MODES = {"none": GD_MODE_NONE, "mask": GD_MODE_MASK, "check": GD_MODE_CHECK, "modulo": GD_MODE_MODULO,
          "maskcount": GD_MODE_MASK_COUNT, "clamp": GD_MODE_CLAMP}
+GD_POLICY_ROUND_ROBIN, GD_POLICY_NO_TENSOR_RANDOM, GD_POLICY_MEMORY_LANE = 0, 1, 2
+POLICIES = {"round_robin": GD_POLICY_ROUND_ROBIN, "no_tensor_random": GD_POLICY_NO_TENSOR_RANDOM,
+            "memory_lane": GD_POLICY_MEMORY_LANE}
 GD_PART_POW2 = 1
 (GD_KIND_COPY, GD_KIND_SAXPY, GD_KIND_GATHER, GD_KIND_SCATTER, GD_KIND_STENCIL, GD_KIND_GEMM) = range(6)
 GD_NUM_KINDS = 6
@@ -39,7 +42,7 @@ EXPORTED = [
     "gd_check_range", "gd_memcpy_h2d", "gd_memcpy_d2h", "gd_memcpy_d2d", "gd_partition_fill",
     "gd_launch_fenced_copy", "gd_launch_fenced_saxpy", "gd_launch_fenced_gather",
     "gd_launch_fenced_scatter", "gd_launch_fenced_stencil", "gd_launch_fenced_gemm",
-    "gd_schedule_round_robin", "gd_launcher_run",
+    "gd_schedule_round_robin", "gd_launcher_run", "gd_launcher_run_policy",
     "gd_stats", "gd_stats_reset", "gd_stats_device_ptr", "gd_status_str", "gd_last_cuda_error", "gd_version",
     "gd_device_flags", "gd_graph_create", "gd_graph_launch", "gd_graph_destroy",
 ]
@@ -102,6 +105,7 @@ def _load():
         "gd_launch_fenced_gemm": [A, u32, i32, u64, u64, u64, u32, u32, u32, u64, u64, u64, vp],
         "gd_schedule_round_robin": [P(gd_work), u32, P(u32)],
         "gd_launcher_run": [A, P(gd_work), u32, P(vp), u32, P(u32)],
+        "gd_launcher_run_policy": [A, P(gd_work), u32, P(vp), u32, u32, P(u32)],
         "gd_stats": [A, u32, P(gd_stats_t)],
         "gd_stats_reset": [A, u32],
         "gd_stats_device_ptr": [A, P(u64)],
@@ -336,11 +340,16 @@ class Arena:
         _chk("gd_graph_create", _lib.gd_graph_create(self._h, arr, len(items), n_streams, ctypes.byref(h)))
         return Graph(h)
 
-    def launcher_run(self, items, streams):
+    def launcher_run(self, items, streams, policy="round_robin"):
+        """gd_launcher_run_policy: policy "round_robin" (the paper's launcher)
+        , "no_tensor_random" (GEMMs never overlap gathers / scatters) or
+        "memory_lane" (memory-bound kernels serialised, GEMMs overlap them)."""
         arr = (gd_work * len(items))(*items)
         sarr = (ctypes.c_void_p * len(streams))(*[_stream(s) for s in streams])
         order = (ctypes.c_uint32 * max(1, len(items)))()
-        _chk("gd_launcher_run", _lib.gd_launcher_run(self._h, arr, len(items), sarr, len(streams), order))
+        pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
+        _chk("gd_launcher_run_policy",
+             _lib.gd_launcher_run_policy(self._h, arr, len(items), sarr, len(streams), pol, order))
         return list(order)[:len(items)]
 
     # statistics -----------------------------------------------------------

@@ -27,8 +27,9 @@ def _bf16_f32(b):
     return (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
 
 
+@pytest.mark.parametrize("policy", ["round_robin", "no_tensor_random", "memory_lane"])
 @pytest.mark.parametrize("mode", ["mask", "check"])
-def test_c5_mixed_tenants(arenas, mode):
+def test_c5_mixed_tenants(arenas, mode, policy):
     a = arenas(8 * PART)
     parts = [a.partition_alloc(PART) for _ in range(8)]
     rng = synth.rng_for(5000)
@@ -57,7 +58,7 @@ def test_c5_mixed_tenants(arenas, mode):
     queue = [it for it in items for _ in range(R)]            # R launches per tenant, FIFO per tenant
     streams = [torch.cuda.Stream() for _ in parts]
     a.stats_reset()
-    order = a.launcher_run(queue, streams)
+    order = a.launcher_run(queue, streams, policy=policy)
     tenants_in_order = [queue[i].tenant for i in order]
     assert tenants_in_order[:8] == list(range(8))               # round robin: one per tenant per round
     torch.cuda.synchronize()
