@@ -19,7 +19,7 @@ def main(path, out):
         name = re.sub(r"<.*>", "", re.sub(r"^.*::", "", r[ki].split("(")[0]))
         m = re.search(r"<(\d)>", r[ki])
         if "<" in r[ki] and m:
-            name += f"<{ {'0': 'none', '1': 'mask', '2': 'check', '3': 'modulo'}[m.group(1)] }>"
+            name += f"<{ {'0': 'none', '1': 'mask', '2': 'check', '3': 'modulo', '4': 'maskcount', '5': 'clamp'}[m.group(1)] }>"
         d = agg.setdefault(name, {"launches": 0, "total_ns": 0.0, "grid": r[gi]})
         d["launches"] += 1
         d["total_ns"] += float(r[vi].replace(",", ""))
