@@ -27,8 +27,15 @@ def main(path, out):
     for d in agg.values():
         d["mean_us"] = round(d["total_ns"] / d["launches"] / 1e3, 2)
         d["share"] = round(d["total_ns"] / tot, 4)
+    # share of each kernel within the timed bench step (C2, mask: one copy and
+    # one saxpy per tenant): what bench.py's roofline.share_of_step measures live
+    step = [k for k in ("k_copy<mask>", "k_saxpy<mask>") if k in agg]
+    step_tot = sum(agg[k]["mean_us"] for k in step)
+    step_share = {k: round(agg[k]["mean_us"] / step_tot, 4) for k in step} if step_tot else {}
     json.dump({"source": path, "note": "ncu --metrics gpu__time_duration.sum --clock-control none; cold-cache, "
-               "serialised launches: compare shares, not absolutes", "kernels": agg}, open(out, "w"), indent=1)
+               "serialised launches: compare shares, not absolutes", "step_share_c2_mask": step_share,
+               "kernels": agg}, open(out, "w"), indent=1)
+    print("share within the C2 mask step:", step_share)
     for k, d in agg.items():
         print(f"{k:24s} n={d['launches']:5d} mean={d['mean_us']:10.2f} us share={d['share']:.3f} grid={d['grid']}")
 
