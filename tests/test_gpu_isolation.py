@@ -26,7 +26,7 @@ MiB = 1 << 20
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("mode", ["mask", "modulo"])
+@pytest.mark.parametrize("mode", ["mask", "modulo", "clamp", "maskcount"])
 def test_no_foreign_reads(arenas, mode):
     a = arenas(4 * 16 * MiB)
     parts = [a.partition_alloc(16 * MiB) for _ in range(4)]
@@ -63,7 +63,7 @@ def _sanitize(mode):
     return subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
 
 
-@pytest.mark.parametrize("mode", ["mask", "modulo", "check"])
+@pytest.mark.parametrize("mode", ["mask", "modulo", "check", "maskcount", "clamp"])
 def test_sanitizer_clean_when_fenced(mode):
     r = _sanitize(mode)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
