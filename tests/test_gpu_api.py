@@ -95,3 +95,30 @@ def test_streams_from_torch_and_async(arenas):
     s.synchronize()
     assert np.array_equal(download(p.base + 16 * MiB, 8 * MiB), download(p.base, 8 * MiB))
     assert a.device_flags() == 0
+
+
+@pytest.mark.parametrize("mode", ["none", "mask", "check", "modulo", "maskcount", "clamp"])
+def test_degenerate_launches_do_nothing(arenas, mode):
+    """Empty and degenerate shapes (n = 0 is GD_OK and does
+    nothing): no byte of the arena changes and nothing is counted, in every
+    mode -- including pointers far outside the partition, which an empty
+    launch must not even fence."""
+    a = arenas(2 * 16 * MiB)
+    parts = [a.partition_alloc(16 * MiB) for _ in range(2)]
+    for p in parts:
+        upload(p.base, np.full(p.size, 0xA5, np.uint8))
+    before = download(a.base, a.size)
+    p, far = parts[1], 1 << 46
+    a.stats_reset()
+    a.copy(p.id, mode, far, far, 0)
+    a.saxpy(p.id, mode, 2.0, far, far, 0)
+    a.gather(p.id, mode, far, far, far, 0)
+    a.gather(p.id, mode, far, far, far, 0, 32)
+    a.scatter(p.id, mode, far, far, far, 0)
+    a.stencil(p.id, mode, far, far, 2, 100, 100, 0.5, 0.125)       # H < 3: no interior point
+    a.stencil(p.id, mode, far, far, 100, 2, 100, 0.5, 0.125)       # W < 3
+    a.gemm(p.id, mode, far, far, far, 0, 256, 64, 64, 64, 256)       # M = 0
+    a.gemm(p.id, mode, far, far, far, 128, 0, 64, 64, 64, 64)        # N = 0
+    torch.cuda.synchronize()
+    assert np.array_equal(download(a.base, a.size), before)
+    assert a.stats(p.id)["violations"] == 0
