@@ -122,3 +122,34 @@ def test_degenerate_launches_do_nothing(arenas, mode):
     torch.cuda.synchronize()
     assert np.array_equal(download(a.base, a.size), before)
     assert a.stats(p.id)["violations"] == 0
+
+
+def test_wrap_caller_owned_torch_memory():
+    """gd_arena_wrap over a torch allocation (the caller
+    keeps the tensor alive, the library never frees it): partitions carve the
+    borrowed range, are scrubbed, and fence like VMM partitions (mask copy
+    crossing the end wraps to the partition start, bit-exact vs the oracle)."""
+    import oracle
+    S = 16 * MiB
+    buf = torch.empty(2 * S, dtype=torch.uint8, device="cuda")
+    base = (buf.data_ptr() + S - 1) & ~(S - 1)
+    with g.Arena.wrap(0, base, S) as a:
+        parts = [a.partition_alloc(S // 4) for _ in range(4)]
+        assert [p.base for p in parts] == [base + t * (S // 4) for t in range(4)]
+        assert (download(base, S) == 0).all()                      # scrubbed (reading A15)
+        rng = synth.rng_for(77)
+        p = parts[2]
+        data = synth.random_bytes(rng, 1 * MiB)
+        upload(p.base, data)
+        before = download(base, S)
+        n, over = 512 * 1024 + 48, 4096 + 32
+        dst = p.end - (n - over)
+        a.copy(p.id, "mask", dst, p.base, n)
+        torch.cuda.synchronize()
+        mem = oracle.Mem(p.base, buf=before[p.base - base:p.base - base + p.size].copy())
+        oracle.copy(mem, p.base, p.size, "mask", dst, p.base, n)
+        after = download(base, S)
+        assert np.array_equal(after[p.base - base:p.base - base + p.size], mem.buf)
+        lo, hi = p.base - base, p.base - base + p.size
+        assert np.array_equal(after[:lo], before[:lo]) and np.array_equal(after[hi:], before[hi:])
+    del buf
