@@ -307,6 +307,14 @@ gd_status gd_stats_device_ptr(const gd_arena *a, uint64_t *dev_ptr);
 
 const char *gd_status_str(gd_status s);
 int gd_last_cuda_error(void);
+/* Native kernel for a tenant alone ("When an application runs
+ * alone, the manager issues a native kernel"; SPEC.md:418 --native-when-solo,
+ * default off).  While on and exactly one partition of the arena is live,
+ * every launch is validated in its requested mode and then run as
+ * GD_MODE_NONE: no fence and nothing counted.  A second live partition
+ * restores fencing for the next launch.                                      */
+gd_status gd_arena_set_native_when_solo(gd_arena *a, int on);
+
 /* Synchronises, then reports (and clears) device-side health flags:
  * bit 0 = a tensor-core pipeline wait timed out (the kernel gave up instead
  * of hanging the shared context).                                            */

@@ -135,6 +135,15 @@ gd_status snapshot(gd_arena *a, uint32_t id, uint64_t *base, uint64_t *size) {
 
 bool mul_ok(uint64_t a, uint64_t b, uint64_t *r) { return !__builtin_mul_overflow(a, b, r); }
 
+// native-when-solo is on and exactly one partition is live
+bool solo_native(gd_arena *a) {
+    std::lock_guard<std::mutex> lk(a->mu);
+    if (!a->native_when_solo) return false;
+    uint32_t live = 0;
+    for (uint32_t i = 0; i < GD_MAX_TENANTS; i++) live += a->parts[i].live ? 1u : 0u;
+    return live == 1;
+}
+
 bool tenant_live(gd_arena *a, uint32_t id) {
     std::lock_guard<std::mutex> lk(a->mu);
     return id < GD_MAX_TENANTS && a->parts[id].live;
@@ -479,9 +488,10 @@ namespace gd {
 
 // Validate `w` (dry) or validate and launch it.  Structural errors are
 // returned before anything is issued.
-gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry, bool account, uint64_t *bytes_out,
-                   uint64_t *flops_out) {
+gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool dry, bool account,
+                   uint64_t *bytes_out, uint64_t *flops_out) {
     if (!a) return GD_ERR_INVALID_ARG;
+    gd_work w = w_in;
     if (w.mode > GD_MODE_CLAMP || w.kind >= GD_NUM_KINDS) return GD_ERR_INVALID_ARG;
     uint64_t base, size;
     gd_status st = snapshot(a, w.tenant, &base, &size);
@@ -542,6 +552,10 @@ gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry,
     }
     if (dry || empty) return GD_OK;
     if (a->device < 0) return GD_ERR_UNSUPPORTED;      // virtual arena: bookkeeping only
+    // PAPER.md:175 "when an application runs alone ... issues a native kernel"
+    // (SPEC.md:418 --native-when-solo, off by default): validated as requested,
+    // run unfenced
+    if (w.mode != GD_MODE_NONE && solo_native(a)) w.mode = GD_MODE_NONE;
 
     FenceDesc fd;
     fd.base = base;
@@ -765,6 +779,13 @@ extern "C" const char *gd_status_str(gd_status s) {
 }
 
 extern "C" int gd_last_cuda_error(void) { return g_last_cuda; }
+
+extern "C" gd_status gd_arena_set_native_when_solo(gd_arena *a, int on) {
+    if (!a) return GD_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> lk(a->mu);
+    a->native_when_solo = on != 0;
+    return GD_OK;
+}
 
 extern "C" gd_status gd_device_flags(gd_arena *a, uint32_t *flags) {
     if (!a || !flags) return GD_ERR_INVALID_ARG;

@@ -82,5 +82,6 @@ struct gd_arena {
     uint64_t zero_bytes = 0;
     int sms = 148;
     uint64_t next_gen = 1;
+    bool native_when_solo = false;   // a tenant alone runs the native kernel
     std::mutex mu;
 };

@@ -37,7 +37,7 @@ GD_ALL_TENANTS = 0xFFFFFFFF
 KIND_NAMES = ["copy", "saxpy", "gather", "scatter", "stencil", "gemm"]
 
 EXPORTED = [
-    "gd_arena_create", "gd_arena_wrap", "gd_arena_destroy", "gd_arena_info",
+    "gd_arena_create", "gd_arena_wrap", "gd_arena_destroy", "gd_arena_info", "gd_arena_set_native_when_solo",
     "gd_partition_alloc", "gd_partition_alloc_exact", "gd_partition_free", "gd_partition_get", "gd_malloc", "gd_free",
     "gd_check_range", "gd_memcpy_h2d", "gd_memcpy_d2h", "gd_memcpy_d2d", "gd_partition_fill",
     "gd_launch_fenced_copy", "gd_launch_fenced_saxpy", "gd_launch_fenced_gather",
@@ -84,6 +84,7 @@ def _load():
     sig = {
         "gd_arena_create": [i32, u64, u32, P(vp)],
         "gd_arena_wrap": [i32, u64, u64, P(vp)],
+        "gd_arena_set_native_when_solo": [A, i32],
         "gd_arena_destroy": [A],
         "gd_arena_info": [A, P(u64), P(u64), P(i32)],
         "gd_partition_alloc": [A, u64, P(gd_partition_info)],
@@ -243,6 +244,10 @@ class Arena:
     @property
     def handle(self):
         return self._h
+
+    def set_native_when_solo(self, on: bool) -> None:
+        """a tenant alone runs the native (unfenced) kernel."""
+        _chk("gd_arena_set_native_when_solo", _lib.gd_arena_set_native_when_solo(self._h, int(bool(on))))
 
     def close(self):
         if self._h is not None and self._h.value:

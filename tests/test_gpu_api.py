@@ -140,16 +140,49 @@ def test_wrap_caller_owned_torch_memory():
         rng = synth.rng_for(77)
         p = parts[2]
         data = synth.random_bytes(rng, 1 * MiB)
-        upload(p.base, data)
+        src = p.base + MiB                          # away from [base, base + over), where the tail wraps
+        upload(src, data)
         before = download(base, S)
         n, over = 512 * 1024 + 48, 4096 + 32
         dst = p.end - (n - over)
-        a.copy(p.id, "mask", dst, p.base, n)
+        a.copy(p.id, "mask", dst, src, n)
         torch.cuda.synchronize()
         mem = oracle.Mem(p.base, buf=before[p.base - base:p.base - base + p.size].copy())
-        oracle.copy(mem, p.base, p.size, "mask", dst, p.base, n)
+        oracle.copy(mem, p.base, p.size, "mask", dst, src, n)
         after = download(base, S)
         assert np.array_equal(after[p.base - base:p.base - base + p.size], mem.buf)
         lo, hi = p.base - base, p.base - base + p.size
         assert np.array_equal(after[:lo], before[:lo]) and np.array_equal(after[hi:], before[hi:])
+    del buf
+
+
+def test_native_when_solo():
+    """with native-when-solo on, a tenant alone runs the native
+    kernel (no fence, nothing counted); a second live partition restores
+    fencing.  Run on a wrapped torch buffer so that the unfenced access lands
+    in mapped (unallocated) arena memory, never outside the allocation."""
+    S = 16 * MiB
+    buf = torch.empty(2 * S, dtype=torch.uint8, device="cuda")
+    base = (buf.data_ptr() + S - 1) & ~(S - 1)
+    with g.Arena.wrap(0, base, S) as a:
+        a.set_native_when_solo(True)
+        p = a.partition_alloc(S // 4)                                  # [base, base + 4 MiB)
+        beyond = S // 2                                               # byte offset in the unallocated half
+        upload(base + beyond, np.arange(1024, dtype=np.uint32))
+        j = np.array([(beyond // 4) + 7, 3], dtype=np.int32)          # one index past the partition
+        upload(p.base + MiB, j)
+        a.stats_reset()
+        a.gather(p.id, "check", p.base + 2 * MiB, p.base, p.base + MiB, 2)
+        out = download(p.base + 2 * MiB, 8).view(np.uint32)
+        assert out[0] == 7 and a.stats(p.id)["violations"] == 0     # native: read through, not counted
+        q = a.partition_alloc(S // 4)                                  # a second tenant arrives
+        a.stats_reset()
+        a.gather(p.id, "check", p.base + 2 * MiB, p.base, p.base + MiB, 2)
+        out = download(p.base + 2 * MiB, 8).view(np.uint32)
+        assert out[0] == 0 and a.stats(p.id)["violations"] == 1     # fenced again: refused, counted
+        a.partition_free(q.id)
+        a.set_native_when_solo(False)
+        a.stats_reset()
+        a.gather(p.id, "check", p.base + 2 * MiB, p.base, p.base + MiB, 2)
+        assert a.stats(p.id)["violations"] == 1                      # off: fenced even when alone
     del buf
