@@ -332,11 +332,13 @@ class Workload:
                 s = self.streams[t]
                 for off in (OFF_DST, OFF_Y):
                     a.memcpy_d2h(p.id, host_out.data_ptr(), p.base + off, COPY_BYTES, stream=s)
-            for s in self.streams:
-                s.synchronize()
+            # no host sync between steps: each tenant's stream orders its next
+            # step's uploads after this step's downloads, so consecutive steps
+            # pipeline across the two copy directions
 
         for _ in range(warmup):
             one()
+        torch.cuda.synchronize(self.device)
         barrier()
         torch.cuda.synchronize(self.device)
         t0 = time.perf_counter()
