@@ -105,7 +105,9 @@ extern "C" gd_status gd_launcher_run_policy(gd_arena *a, const gd_work *items, u
     std::vector<std::vector<uint32_t>> queues;
     build_queues(items, n_items, tenants, queues, rank);
     gd_schedule_round_robin(items, n_items, order.data());
-    const bool sep = policy != GD_POLICY_ROUND_ROBIN;
+    // (a virtual arena never launches anything: no events there)
+    const bool sep = policy != GD_POLICY_ROUND_ROBIN && a->device >= 0;
+    const bool lane_on = policy == GD_POLICY_MEMORY_LANE && a->device >= 0;
     ClassEvents ce(sep ? n_streams : 0);
     cudaEvent_t lane = nullptr;                        // MEMORY_LANE: the latest memory-bound kernel
     bool lane_live = false;
@@ -113,7 +115,7 @@ extern "C" gd_status gd_launcher_run_policy(gd_arena *a, const gd_work *items, u
         cudaEvent_t &e;
         ~Guard() { if (e) cudaEventDestroy(e); }
     } guard{lane};
-    if (policy == GD_POLICY_MEMORY_LANE) {
+    if (lane_on) {
         cudaError_t e = cudaEventCreateWithFlags(&lane, cudaEventDisableTiming);
         if (e != cudaSuccess) return gd::cuda_status(e);
     }
@@ -124,13 +126,13 @@ extern "C" gd_status gd_launcher_run_policy(gd_arena *a, const gd_work *items, u
         const int c = class_of(items[i].kind);
         cudaError_t e = cudaSuccess;
         if (sep && c != kStreamCls) e = ce.wait_all(c == kTensorCls ? kRandomCls : kTensorCls, si, s);
-        if (e == cudaSuccess && policy == GD_POLICY_MEMORY_LANE && c != kTensorCls && lane_live)
+        if (e == cudaSuccess && lane_on && c != kTensorCls && lane_live)
             e = cudaStreamWaitEvent(s, lane, 0);
         if (e != cudaSuccess) return gd::cuda_status(e);
         gd_status st = gd::run_work(a, items[i], s, false);
         if (st != GD_OK) return st;
         if (sep && c != kStreamCls) e = ce.record(c, si, s);
-        if (e == cudaSuccess && policy == GD_POLICY_MEMORY_LANE && c != kTensorCls) {
+        if (e == cudaSuccess && lane_on && c != kTensorCls) {
             e = cudaEventRecord(lane, s);
             lane_live = true;
         }

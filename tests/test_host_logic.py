@@ -255,6 +255,30 @@ def test_launcher_validates_all_before_issuing():
     assert a.stats(p.id)["launches"] == 0
 
 
+@pytest.mark.parametrize("policy", ["round_robin", "no_tensor_random", "memory_lane"])
+def test_launcher_policies_validate_before_issuing(policy):
+    """Every issue policy validates all items first (nothing issued, nothing
+    counted on a bad item); an unknown policy is refused before anything."""
+    a = virtual()
+    p = a.partition_alloc(1 << 20)
+    good = g.work(p.id, g.GD_KIND_COPY, "mask", ptr=(p.base, p.base), u64=(0,))
+    bad = g.work(p.id, g.GD_KIND_GEMM, "check", ptr=(p.base, p.base, p.base), u64=(64, 64, 64), u32=(64, 64, 63))
+    with pytest.raises(g.GuardianError) as e:
+        a.launcher_run([good, bad], [None, None], policy=policy)
+    assert e.value.status == g.GD_ERR_UNSUPPORTED
+    assert a.stats(p.id)["launches"] == 0
+    with pytest.raises(g.GuardianError) as e:
+        a.launcher_run([good], [None], policy=7)
+    assert e.value.status == g.GD_ERR_INVALID_ARG
+    a.launcher_run([good], [None], policy=policy)        # n = 0 work: valid, nothing launched
+
+
+def test_native_when_solo_setter():
+    a = virtual()
+    a.set_native_when_solo(True)
+    a.set_native_when_solo(False)
+
+
 def test_exact_partitions_tail_returns_to_pool():
     """gd_partition_alloc_exact: a 12 KiB request takes a
     16 KiB block and gives the 4 KiB tail back, which a later 4 KiB request
