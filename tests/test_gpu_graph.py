@@ -30,7 +30,7 @@ def _toy(arenas):
     return a, parts, toy, host
 
 
-@pytest.mark.parametrize("mode", ["mask", "check"])
+@pytest.mark.parametrize("mode", ["mask", "check", "maskcount", "modulo"])
 def test_graph_replay_matches_oracle(arenas, mode):
     a, parts, toy, host = _toy(arenas)
     items = [g.work(p.id, g.GD_KIND_GATHER, mode, ptr=(p.base + synth.C1_OUT_OFF, p.base, p.base + synth.C1_IDX_OFF),
@@ -48,7 +48,7 @@ def test_graph_replay_matches_oracle(arenas, mode):
     assert np.array_equal(got, mem.buf), first_diff(got, mem.buf)
     st = a.stats()
     assert st["launches"] == 3 * len(items)
-    assert st["violations"] == (3 * toy.n_planted if mode == "check" else 0)
+    assert st["violations"] == (3 * toy.n_planted if mode in ("check", "maskcount") else 0)
     graph.close()
 
 
