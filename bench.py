@@ -30,6 +30,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 GiB = 1 << 30
+MiB = 1 << 20
 # fence modes in gd_mode order; the unfenced twin first (overheads are against it)
 ALL_MODES = ("none", "mask", "check", "modulo", "maskcount", "clamp")
 TENANTS = 8
@@ -464,6 +465,7 @@ def run_gpu(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(seconds=args.cpu_seconds)
+        cpu["by_config"] = cpu_by_config("mask", host_threads(), table)
 
     if rank == 0:
         line = {
@@ -553,6 +555,143 @@ def cpu_baseline(seconds: float = 12.0, mode: str = "mask"):
     return {"value": round(passes * s.bytes_per_pass / el / 1e9, 3), "unit": "GB/s", "cores": th, "kind": "oracle",
             "sample": f"{passes} pass(es) x {th} tenants x (64 MiB copy + 2^24-element saxpy), mode={mode}, "
                       f"{el:.1f} s"}
+
+
+# ---------------------------------------------------------------------------
+# cpu_baseline leg, per BASELINE config (SURVEY.md §8(d) "Oracle timing"):
+# the oracle as it stands on a bounded sample of every config, one tenant per
+# host thread, and the GPU/oracle ratio against this run's own kernel table.
+# ---------------------------------------------------------------------------
+OBASE = 0x7F0000000000
+
+
+def _oimports():
+    import numpy as np
+    import oracle
+    import synth
+    return np, oracle, synth
+
+
+def _otimed(fn, th):
+    from concurrent.futures import ThreadPoolExecutor
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(th) as ex:
+        list(ex.map(fn, range(th)))
+    return time.perf_counter() - t0
+
+
+def _ocfg_c1(mode):
+    np, oracle, synth = _oimports()
+    g = synth.toy_gather()
+    m = oracle.Mem(OBASE, synth.C1_ARENA)
+    for t in range(synth.C1_TENANTS):
+        b = OBASE + t * synth.C1_PART
+        m.write(b + synth.C1_TABLE_OFF, g.tables[t])
+        m.write(b + synth.C1_IDX_OFF, g.idx[t])
+    t0 = time.perf_counter()
+    for t in range(synth.C1_TENANTS):
+        b = OBASE + t * synth.C1_PART
+        oracle.gather(m, b, synth.C1_PART, mode, b + synth.C1_OUT_OFF, b + synth.C1_TABLE_OFF, b + synth.C1_IDX_OFF,
+                      synth.C1_N, 1)
+    el = time.perf_counter() - t0
+    n = synth.C1_TENANTS * synth.C1_N
+    return {"sample": f"whole C1: {n} indices, 4 tenants, one thread", "seconds": round(el, 3),
+            "GB/s": round(12 * n / el / 1e9, 4), "cores": 1}
+
+
+def _ocfg_c2(mode, th):
+    np, oracle, synth = _oimports()
+    cp, sx = 64 * MiB, 1 << 24
+    mems = []
+    for t in range(th):
+        b = OBASE + t * PART
+        m = oracle.Mem(b, 4 * cp)
+        rng = synth.rng_for(2000 + t)
+        m.buf[:cp] = synth.random_bytes(rng, cp)
+        m.write(b + 2 * cp, synth.uniform_f32(rng, sx))
+        m.write(b + 3 * cp, synth.uniform_f32(rng, sx))
+        mems.append((m, b))
+
+    def one(i):
+        m, b = mems[i]
+        oracle.copy(m, b, PART, mode, b + cp, b, cp)
+        oracle.saxpy(m, b, PART, mode, 1.5, b + 2 * cp, b + 3 * cp, sx)
+    el = _otimed(one, th)
+    return {"sample": f"{th} tenants x (64 MiB copy + 2^24-element saxpy)", "seconds": round(el, 3),
+            "GB/s": round(th * (2 * cp + 12 * sx) / el / 1e9, 3), "cores": th}
+
+
+def _ocfg_c3(mode, th):
+    np, oracle, synth = _oimports()
+    T, n = 1 << 26, 1 << 22
+    mems = []
+    for t in range(th):
+        b = OBASE + t * PART
+        m = oracle.Mem(b, 4 * T + 8 * n)
+        rng = synth.rng_for(3000 + t)
+        m.write(b, rng.integers(0, 2**32, T, dtype=np.uint64).astype(np.uint32))
+        j = rng.integers(0, T, n, dtype=np.int64)
+        pos = synth.planted_positions(rng, n, synth.planted_count(0.01, n))
+        j[pos] = rng.integers(-2**31, 0, len(pos))
+        m.write(b + 4 * T, j.astype(np.int32))
+        mems.append((m, b))
+
+    def one(i):
+        m, b = mems[i]
+        oracle.gather(m, b, PART, mode, b + 4 * T + 4 * n, b, b + 4 * T, n, 1)
+    el = _otimed(one, th)
+    return {"sample": f"{th} tenants x 2^22 indices into a 2^26-word table, 1 % planted OOB",
+            "seconds": round(el, 3), "GB/s": round(th * 12 * n / el / 1e9, 3), "cores": th}
+
+
+def _ocfg_c4_gemm(mode):
+    np, oracle, synth = _oimports()
+    n, rows = 8192, 16
+    b = OBASE
+    m = oracle.Mem(b, 3 * n * n * 2)
+    rng = synth.rng_for(4006)
+    m.write(b, synth.bf16_bits_uniform(rng, n * n))
+    m.write(b + n * n * 2, synth.bf16_bits_uniform(rng, n * n))
+    sel = np.sort(rng.permutation(n)[:rows]).astype(np.uint32)
+    t0 = time.perf_counter()
+    oracle.gemm(m, b, PART, mode, b + 2 * n * n * 2, b, b + n * n * 2, n, n, n, n, n, n, rows=sel)
+    el = time.perf_counter() - t0
+    return {"sample": f"{rows} seeded full rows of C at 8192^3, one thread", "seconds": round(el, 3),
+            "TFLOP/s": round(2 * rows * n * n / el / 1e12, 6), "cores": 1}
+
+
+def _ocfg_c4_stencil(mode, th):
+    np, oracle, synth = _oimports()
+    H = W = 2048
+    mems = []
+    for t in range(th):
+        b = OBASE + t * PART
+        m = oracle.Mem(b, 8 * H * W)
+        m.write(b, synth.uniform_f32(synth.rng_for(4100 + t), H * W, 0.0, 1.0))
+        mems.append((m, b))
+
+    def one(i):
+        m, b = mems[i]
+        oracle.stencil(m, b, PART, mode, b + 4 * H * W, b, H, W, W, 0.5, 0.125)
+    el = _otimed(one, th)
+    return {"sample": f"{th} tenants x 2048^2 stencil", "seconds": round(el, 3),
+            "GB/s": round(th * 8 * (H - 2) * (W - 2) / el / 1e9, 3), "cores": th}
+
+
+
+def cpu_by_config(mode, th, table=None):
+    out = {"C1_toy_gather": _ocfg_c1(mode), "C2_copy_saxpy": _ocfg_c2(mode, th), "C3_gather": _ocfg_c3(mode, th),
+           "C4_gemm": _ocfg_c4_gemm(mode), "C4_stencil": _ocfg_c4_stencil(mode, th)}
+    if table:
+        pick = {"C2_copy_saxpy": (("copy_4GiB", "saxpy_2^30"), "GB/s"), "C3_gather": (("gather_2^26_1pct_oob",), "GB/s"),
+                "C4_gemm": (("gemm_8192^3",), "TFLOP/s"), "C4_stencil": (("stencil_32768^2",), "GB/s")}
+        for k, (names, unit) in pick.items():
+            vals = [table[n][mode][unit] for n in names if n in table and mode in table[n]]
+            if vals:
+                gpu = sum(vals) / len(vals)
+                out[k]["gpu"] = gpu
+                out[k]["gpu_over_oracle"] = round(gpu / out[k][unit], 1)
+    return out
 
 
 def run_reference(args):
