@@ -91,6 +91,8 @@ def lib():
         L.or_gather.argtypes = [P, u64, u64, u64, u64, u32]
         L.or_scatter_add.argtypes = [P, u64, u64, u64, u64]
         L.or_stencil.argtypes = [P, u64, u64, u32, u32, u64, f32, f32]
+        L.or_stencil_tma.argtypes = [P, u64, u64, u32, u32, u64, f32, f32]
+        L.or_stencil_tma.restype = None
         L.or_desc_rows.restype = u64
         L.or_desc_rows.argtypes = [P, u64, u64, u64, u64, ctypes.POINTER(u64)]
         L.or_gemm.argtypes = [P, u64, u64, u64, u32, u32, u32, u64, u64, u64,
@@ -238,6 +240,10 @@ def scatter_add(mem, base, size, mode, table, idx, src, n) -> Counts:
 
 def stencil(mem, base, size, mode, out, inp, H, W, pitch, c0, c1) -> Counts:
     return _run(lib().or_stencil, mem, base, size, mode, out, inp, H, W, pitch, c0, c1)
+
+
+def stencil_tma(mem, base, size, mode, out, inp, H, W, pitch, c0, c1) -> Counts:
+    return _run(lib().or_stencil_tma, mem, base, size, mode, out, inp, H, W, pitch, c0, c1)
 
 
 def desc_rows(base, size, mode, p, rows, rowbytes, stride):

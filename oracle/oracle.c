@@ -264,6 +264,50 @@ uint64_t or_desc_rows(const or_ctx *c, uint64_t p, uint64_t rows,
     return valid < rows ? valid : rows;
 }
 
+/* K5 v2, the TMA-staged stencil:
+ * both operands are descriptor-fenced.  `in` is H rows of W floats (`pitch`
+ * floats apart), `out` the H-1 rows of W-1 floats that can hold interior
+ * points (rows 0..H-2, columns 0..W-2; row 0 and column 0 are never stored).
+ * Rows of `in` at or past its descriptor row count read as 0 (TMA OOB fill),
+ * interior points of `out` rows at or past its row count are not stored (TMA
+ * store clipping).  Arithmetic and order exactly as or_stencil.  The counting
+ * modes count the rows check would refuse, once per operand.                */
+void or_stencil_tma(or_ctx *c, uint64_t out, uint64_t in, uint32_t H, uint32_t W,
+                    uint64_t pitch, float c0, float c1) {
+    if (H < 3 || W < 3) return;
+    uint64_t inf, outf;
+    uint64_t rin = or_desc_rows(c, in, H, 4ull * W, 4ull * pitch, &inf);
+    uint64_t rout = or_desc_rows(c, out, H - 1, 4ull * (W - 1), 4ull * pitch, &outf);
+    if (c->mode == OR_CHECK || c->mode == OR_MASK_COUNT || c->mode == OR_CLAMP) {
+        or_ctx chk = *c;
+        uint64_t pf;
+        chk.mode = OR_CHECK;
+        c->violations += (H - or_desc_rows(&chk, in, H, 4ull * W, 4ull * pitch, &pf)) +
+                         ((H - 1) - or_desc_rows(&chk, out, H - 1, 4ull * (W - 1), 4ull * pitch, &pf));
+    }
+    for (uint64_t r = 1; r + 1 < H; r++) {
+        for (uint64_t col = 1; col + 1 < W; col++) {
+            float v[5] = {0.f, 0.f, 0.f, 0.f, 0.f};          /* C, N, S, W, E */
+            const uint64_t rr[5] = {r, r - 1, r + 1, r, r};
+            const uint64_t cc[5] = {col, col, col, col - 1, col + 1};
+            for (int k = 0; k < 5; k++) {
+                if (rr[k] >= rin) continue;                   /* past the descriptor: zero fill */
+                uint8_t *p = mem_at(c, inf + 4 * (rr[k] * pitch + cc[k]), 4);
+                if (p) memcpy(&v[k], p, 4);
+            }
+            float ns = v[1] + v[2];
+            float we = v[3] + v[4];
+            float s = ns + we;
+            float t = c0 * v[0];
+            float o = fmaf(c1, s, t);
+            if (r < rout) {
+                uint8_t *p = mem_at(c, outf + 4 * (r * pitch + col), 4);
+                if (p) memcpy(p, &o, 4);
+            }
+        }
+    }
+}
+
 uint16_t or_f32_to_bf16(float f) {
     uint32_t u;
     memcpy(&u, &f, 4);

@@ -140,6 +140,13 @@ void or_gemm(or_ctx *c, uint64_t C, uint64_t A, uint64_t B, uint32_t M,
              uint32_t N, uint32_t K, uint64_t lda, uint64_t ldb, uint64_t ldc,
              const uint32_t *rows, uint32_t nrows);
 
+/* K5 v2: the stencil with both operands descriptor-fenced (TMA staging).
+ * in: H rows x W floats; out: rows 0..H-2 x columns 0..W-2 (interior points
+ * only are stored).  Rows of in past its descriptor row count read as 0;
+ * interior points in out rows past its row count are not stored.             */
+void or_stencil_tma(or_ctx *c, uint64_t out, uint64_t in, uint32_t H, uint32_t W,
+                    uint64_t pitch, float c0, float c1);
+
 /* bf16 helpers used by or_gemm (exposed for pins).                           */
 uint16_t or_f32_to_bf16(float f);
 float or_bf16_to_f32(uint16_t h);
