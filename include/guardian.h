@@ -220,6 +220,19 @@ gd_status gd_launch_fenced_scatter(gd_arena *a, uint32_t id, gd_mode mode, uint6
 gd_status gd_launch_fenced_stencil(gd_arena *a, uint32_t id, gd_mode mode, uint64_t out, uint64_t in,
                                    uint32_t H, uint32_t W, uint64_t pitch_elems, float c0, float c1,
                                    void *stream);
+/* K5 v2: the same sweep with both operands
+ * staged by TMA and fenced in their tensor maps (reading R-TMA) instead of
+ * per access: `in` is H rows x W floats, `out` the rows 0..H-2 x columns
+ * 0..W-2 that hold interior points.  Each map's base is fenced like a
+ * 16-byte access (check: an illegal base gives no rows) and its row count
+ * clamped so that its last row ends inside the partition; rows of `in` past
+ * it read as 0, interior points in rows of `out` past it are not stored (no
+ * wrap-around of rows, unlike v1's per-access mask).  The counting modes
+ * count, once per operand, the rows check would refuse.  Same alignment
+ * rules as gd_launch_fenced_stencil.                                         */
+gd_status gd_launch_fenced_stencil_tma(gd_arena *a, uint32_t id, gd_mode mode, uint64_t out, uint64_t in,
+                                       uint32_t H, uint32_t W, uint64_t pitch_elems, float c0, float c1,
+                                       void *stream);
 /* C[M,N] = A[M,K] . B[N,K]^T, bf16 inputs (K-major, row strides lda/ldb in
  * elements), fp32 accumulation on the tcgen05 tensor cores, bf16 output
  * (row stride ldc).  The fence is applied to the TMA tensor maps: each

@@ -533,6 +533,7 @@ gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool d
             const uint64_t pitch = w.u64[0], H = w.u32[0], W = w.u32[1];
             if ((w.ptr[0] | w.ptr[1]) % 16 || pitch % 4) return GD_ERR_ALIGN;
             if (pitch < W || !mul_ok(H, pitch, &t) || t > (1ull << 58)) return GD_ERR_INVALID_ARG;
+            if (w.u32[2] > 1) return GD_ERR_INVALID_ARG;          // 0: K5 v1 (LSU), 1: K5 v2 (TMA)
             empty = H < 3 || W < 3;
             bytes = empty ? 0 : 8 * (H - 2) * (W - 2);
             flops = empty ? 0 : 5 * (H - 2) * (W - 2);
@@ -585,8 +586,13 @@ gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool d
             e = launch_scatter(w.mode, fd, w.ptr[0], w.ptr[1], w.ptr[2], w.u64[0], stream, g);
             break;
         case GD_KIND_STENCIL:
-            e = launch_stencil(w.mode, fd, w.ptr[0], w.ptr[1], w.u32[0], w.u32[1], w.u64[0], w.f32[0], w.f32[1],
-                               stream, g);
+            if (w.u32[2] == 1) {
+                st = stencil_tma_dispatch(a, w, base, size, stream, g);
+                if (st != GD_OK) return st;
+            } else {
+                e = launch_stencil(w.mode, fd, w.ptr[0], w.ptr[1], w.u32[0], w.u32[1], w.u64[0], w.f32[0], w.f32[1],
+                                   stream, g);
+            }
             break;
         case GD_KIND_GEMM: {
             st = gemm_dispatch(a, w, base, size, stream, g);
@@ -679,6 +685,21 @@ extern "C" gd_status gd_launch_fenced_stencil(gd_arena *a, uint32_t id, gd_mode 
     w.ptr[1] = in;
     w.u32[0] = H;
     w.u32[1] = W;
+    w.u64[0] = pitch_elems;
+    w.f32[0] = c0;
+    w.f32[1] = c1;
+    return run_work(a, w, (cudaStream_t)stream, false);
+}
+
+extern "C" gd_status gd_launch_fenced_stencil_tma(gd_arena *a, uint32_t id, gd_mode mode, uint64_t out,
+                                                  uint64_t in, uint32_t H, uint32_t W, uint64_t pitch_elems, float c0,
+                                                  float c1, void *stream) {
+    gd_work w = mk(id, GD_KIND_STENCIL, mode);
+    w.ptr[0] = out;
+    w.ptr[1] = in;
+    w.u32[0] = H;
+    w.u32[1] = W;
+    w.u32[2] = 1;
     w.u64[0] = pitch_elems;
     w.f32[0] = c0;
     w.f32[1] = c1;

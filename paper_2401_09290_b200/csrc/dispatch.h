@@ -16,6 +16,12 @@ gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry,
 gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t size, cudaStream_t stream,
                         const Geom &g);
 gd_status gemm_prepare(gd_arena *a, const gd_work &w, uint64_t base, uint64_t size);
+// K5 v2: the stencil with both operands staged by TMA (k_stencil_tma.cu).
+gd_status stencil_tma_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t size, cudaStream_t stream,
+                               const Geom &g);
+gd_status stencil_tma_prepare(gd_arena *a, const gd_work &w, uint64_t base, uint64_t size);
+// Trusted all-zero buffer of >= 2K bytes outside every partition (gemm.cu).
+gd_status ensure_zero_row(gd_arena *a, uint64_t K);
 gd_status cuda_status(cudaError_t e);
 // Bounds-table snapshot of one partition: base, size and its generation
 // (bumped at every allocation, so a freed-and-reused id is detected).

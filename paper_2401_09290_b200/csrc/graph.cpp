@@ -60,8 +60,9 @@ extern "C" gd_status gd_graph_create(gd_arena *a, const gd_work *items, uint32_t
         bool seen = false;
         for (auto &u : g->uses) seen = seen || u.id == items[i].tenant;
         if (!seen) g->uses.push_back({items[i].tenant, gen});
-        if (items[i].kind == GD_KIND_GEMM) {
-            st = gd::gemm_prepare(a, items[i], base, size);
+        if (items[i].kind == GD_KIND_GEMM || (items[i].kind == GD_KIND_STENCIL && items[i].u32[2] == 1)) {
+            st = items[i].kind == GD_KIND_GEMM ? gd::gemm_prepare(a, items[i], base, size)
+                                               : gd::stencil_tma_prepare(a, items[i], base, size);
             if (st != GD_OK) {
                 destroy(g);
                 return st;

@@ -41,7 +41,7 @@ EXPORTED = [
     "gd_partition_alloc", "gd_partition_alloc_exact", "gd_partition_free", "gd_partition_get", "gd_malloc", "gd_free",
     "gd_check_range", "gd_memcpy_h2d", "gd_memcpy_d2h", "gd_memcpy_d2d", "gd_partition_fill",
     "gd_launch_fenced_copy", "gd_launch_fenced_saxpy", "gd_launch_fenced_gather",
-    "gd_launch_fenced_scatter", "gd_launch_fenced_stencil", "gd_launch_fenced_gemm",
+    "gd_launch_fenced_scatter", "gd_launch_fenced_stencil", "gd_launch_fenced_stencil_tma", "gd_launch_fenced_gemm",
     "gd_schedule_round_robin", "gd_launcher_run", "gd_launcher_run_policy",
     "gd_stats", "gd_stats_reset", "gd_stats_device_ptr", "gd_status_str", "gd_last_cuda_error", "gd_version",
     "gd_device_flags", "gd_graph_create", "gd_graph_launch", "gd_graph_destroy",
@@ -103,6 +103,7 @@ def _load():
         "gd_launch_fenced_gather": [A, u32, i32, u64, u64, u64, u64, u32, vp],
         "gd_launch_fenced_scatter": [A, u32, i32, u64, u64, u64, u64, vp],
         "gd_launch_fenced_stencil": [A, u32, i32, u64, u64, u32, u32, u64, f32, f32, vp],
+        "gd_launch_fenced_stencil_tma": [A, u32, i32, u64, u64, u32, u32, u64, f32, f32, vp],
         "gd_launch_fenced_gemm": [A, u32, i32, u64, u64, u64, u32, u32, u32, u64, u64, u64, vp],
         "gd_schedule_round_robin": [P(gd_work), u32, P(u32)],
         "gd_launcher_run": [A, P(gd_work), u32, P(vp), u32, P(u32)],
@@ -332,6 +333,12 @@ class Arena:
         _chk("gd_launch_fenced_stencil",
              _lib.gd_launch_fenced_stencil(self._h, pid, _mode(mode), out, inp, H, W, pitch, c0, c1,
                                            _stream(stream)))
+
+    def stencil_tma(self, pid, mode, out, inp, H, W, pitch, c0, c1, stream=None):
+        """K5 v2: both operands TMA-staged and descriptor-fenced."""
+        _chk("gd_launch_fenced_stencil_tma",
+             _lib.gd_launch_fenced_stencil_tma(self._h, pid, _mode(mode), out, inp, H, W, pitch, c0, c1,
+                                               _stream(stream)))
 
     def gemm(self, pid, mode, C, A, B, M, N, K, lda, ldb, ldc, stream=None):
         _chk("gd_launch_fenced_gemm",
