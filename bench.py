@@ -290,6 +290,9 @@ class Workload:
                                       16 * n_idx, "GB/s"),
             "stencil_32768^2": (lambda m, s: a.stencil(p5.id, m, p5.base + 8 * GiB, p5.base + 4 * GiB, H, W, W,
                                                        0.5, 0.125, stream=s), 8 * (H - 2) * (W - 2), "GB/s"),
+            "stencil_tma_32768^2": (lambda m, s: a.stencil_tma(p5.id, m, p5.base + 8 * GiB, p5.base + 4 * GiB, H, W,
+                                                               W, 0.5, 0.125, stream=s), 8 * (H - 2) * (W - 2),
+                                    "GB/s"),
             "gemm_8192^3": (lambda m, s: a.gemm(p6.id, m, p6.base + 2 * n * n * 2, p6.base, p6.base + n * n * 2,
                                                 n, n, n, n, n, n, stream=s), 2 * n ** 3, "TFLOP/s"),
         }

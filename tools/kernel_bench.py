@@ -194,6 +194,14 @@ def main():
                        args.reps)
         results["stencil_32768^2"] = summarize("stencil 32768^2", r, 8 * (H - 2) * (W - 2), "GB/s", hbm)
 
+    if want("stencil_tma"):
+        H = W = 32768
+        devmem.view(b + 4 * GiB, H * W, torch.float32).uniform_(0, 1, generator=gen)
+        r = time_modes(lambda m, s: arena.stencil_tma(p.id, m, b + 8 * GiB, b + 4 * GiB, H, W, W, 0.5, 0.125,
+                                                      stream=s), args.reps)
+        results["stencil_tma_32768^2"] = summarize("stencil v2 (TMA) 32768^2", r, 8 * (H - 2) * (W - 2), "GB/s",
+                                                   hbm)
+
     if only is not None and "l2" in only:
         # L2-resident working sets (< 126 MB L2), where the
         # fence's ALU cost is least hidden (the paper's all-cache-hit worst case,

@@ -54,6 +54,8 @@ def main():
             ar.gather(p.id, a.mode, b + 3 * GiB, b, b + 2 * GiB + GiB // 2, n_rows, a.D)
         elif a.kind == "scatter":
             ar.scatter(p.id, a.mode, b, b + 2 * GiB, b + 2 * GiB + GiB // 4, 1 << 26)
+        elif a.kind == "stencil_tma":
+            ar.stencil_tma(p.id, a.mode, b + 8 * GiB, b + 4 * GiB, 32768, 32768, 32768, 0.5, 0.125)
         elif a.kind == "stencil":
             ar.stencil(p.id, a.mode, b + 8 * GiB, b + 4 * GiB, 32768, 32768, 32768, 0.5, 0.125)
         elif a.kind == "gemm":
