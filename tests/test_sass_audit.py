@@ -52,6 +52,14 @@ def test_gemm_uses_tcgen05_and_tma(sass):
     assert any(i.startswith("UTMALDG.2D.2CTA") for i in sass["k_gemm2"])
 
 
+def test_stencil_v2_is_tma_staged(sass):
+    """K5 v2 moves its tiles with TMA (load and store) and has no per-access
+    global load or store besides the <= 3 tail columns."""
+    ins = sass["k_stencil_tma"]
+    assert count(ins, r"UTMALDG") >= 1 and count(ins, r"UTMASTG") >= 1
+    assert count(ins, r"LDG") == 0
+
+
 @pytest.mark.parametrize("kernel", ["k_copy", "k_saxpy", "k_gather1", "k_scatter", "k_stencil"])
 def test_fenced_variants_carry_fence_logic(sass, kernel):
     def variant(m):        # k_x<m> or k_x<m, ...> (first instantiation)

@@ -43,6 +43,9 @@ def main():
         a.saxpy(p.id, args.mode, 0.5, p.base + 8 * MiB, src, 16 * 1024)                  # y elsewhere
         a.stencil(p.id, args.mode, src, p.base + 8 * MiB, 40, 200, 200, 0.5, 0.125)       # out elsewhere
         a.stencil(p.id, args.mode, p.base + 8 * MiB, src, 40, 200, 200, 0.5, 0.125)       # in elsewhere
+        if args.mode != "none":                    # unfenced TMA would fault the context outright
+            a.stencil_tma(p.id, args.mode, src, p.base + 8 * MiB, 40, 203, 204, 0.5, 0.125)
+            a.stencil_tma(p.id, args.mode, p.base + 8 * MiB, src, 40, 203, 204, 0.5, 0.125)
     if args.mode != "none":                        # the unfenced GEMM's TMA would fault the context outright
         for src in (parts[0].base + 4096, far):
             a.gemm(p.id, args.mode, p.base + 10 * MiB, src, p.base + 12 * MiB, 256, 256, 128, 128, 128, 256)

@@ -1,5 +1,5 @@
 """One small fenced GEMM on each path (2-SM for >= 256 rows, 1-SM below) and
-one stencil, for compute-sanitizer racecheck / synccheck runs (dev tool):
+both stencils, for compute-sanitizer racecheck / synccheck runs (dev tool):
   compute-sanitizer --tool racecheck python tools/gemm_small.py
 """
 import os
@@ -24,6 +24,7 @@ def main():
         a.gemm(p.id, "mask", p.base + 8 * MiB, p.base, p.base + 2 * MiB, M, 256, 256, 256, 256, 256)
     devmem.view(p.base + 4 * MiB, 1 << 20, torch.float32).uniform_(0, 1, generator=gen)
     a.stencil(p.id, "check", p.base + 12 * MiB, p.base + 4 * MiB, 200, 1000, 1024, 0.5, 0.125)
+    a.stencil_tma(p.id, "check", p.base + 12 * MiB, p.base + 4 * MiB, 200, 1001, 1024, 0.5, 0.125)
     torch.cuda.synchronize()
     print("flags", a.device_flags())
 
