@@ -174,6 +174,34 @@ def test_c4_stencil_full_sampled_rows(arenas):
         np.testing.assert_array_equal(got, want, err_msg=f"row {r}")
 
 
+def test_c4_stencil_v2_full_sampled_rows(arenas):
+    """K5 v2 at the BASELINE size in the bench's launch configuration: sampled
+    rows (incl. tile edges at 16-row and 248-column boundaries) against the
+    oracle's or_stencil_tma on the 3-row band, and the boundary columns kept."""
+    a = arenas(PART)
+    p = a.partition_alloc(PART)
+    H = W = 32768
+    inp, out = p.base + 4 * GiB, p.base + 8 * GiB
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(4001)
+    devmem.view(inp, H * W, torch.float32).uniform_(0, 1, generator=gen)
+    devmem.view(out, H * W, torch.float32).fill_(-3.0)
+    a.stencil_tma(p.id, "mask", out, inp, H, W, W, 0.5, 0.125)
+    rng = synth.rng_for(10)
+    rows = np.concatenate([[1, 2, 16, 17, 18, H - 2], rng.integers(1, H - 1, 20)])
+    for r in rows:
+        band = download(inp + 4 * (int(r) - 1) * W, 3 * 4 * W)
+        m = oracle.Mem(0x20000000, 4 << 20)
+        m.buf[:band.size] = band
+        oracle.stencil_tma(m, 0x20000000, 4 << 20, "none", 0x20000000 + (2 << 20), 0x20000000, 3, W, W, 0.5, 0.125)
+        want = m.view(0x20000000 + (2 << 20) + 4 * W, np.uint32, W)[1:W - 1]
+        row = download(out + 4 * int(r) * W, 4 * W).view(np.float32)
+        np.testing.assert_array_equal(row.view(np.uint32)[1:W - 1], want, err_msg=f"row {r}")
+        assert row[0] == -3.0 and row[W - 1] == -3.0                   # boundary columns untouched
+    for r in (0, H - 1):
+        assert (download(out + 4 * r * W, 4 * W).view(np.float32) == -3.0).all()
+
+
 @pytest.mark.parametrize("clamp", [False, True])
 def test_c4_gemm_8192_sampled_rows(arenas, clamp):
     a = arenas(PART)
