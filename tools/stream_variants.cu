@@ -111,13 +111,62 @@ static int occ(K k) {
     return b;
 }
 
-extern "C" int variant_count() { return 14; }
+// TMA bulk copy (cp.async.bulk, no tensor map): each CTA moves NB buffers of
+// BYTES through shared memory; one thread issues, an mbarrier collects the
+// loads, bulk stores drain from shared memory.
+template <int NB, int BYTES>
+__global__ void __launch_bounds__(32) v_bulk(F f, uint64_t dst, uint64_t src, uint64_t nvec) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + NB * BYTES);
+    const uint64_t nbytes = nvec * 16, per = (uint64_t)NB * BYTES;
+    const uint64_t o = (uint64_t)blockIdx.x * per;
+    if (threadIdx.x != 0 || o >= nbytes) return;
+    const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint64_t len = nbytes - o < per ? nbytes - o : per;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"((uint32_t)len) : "memory");
+    for (int b = 0; b < NB; b++) {
+        const uint64_t ob = o + (uint64_t)b * BYTES;
+        if (ob >= nbytes) break;
+        const uint32_t sz = (uint32_t)(nbytes - ob < (uint64_t)BYTES ? nbytes - ob : BYTES);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(sm + b * BYTES)),
+                     "l"(f(src + ob)), "r"(sz), "r"(bar_s)
+                     : "memory");
+    }
+    asm volatile("{\n\t.reg .pred p;\n\tW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W;\n\t}" ::"r"(
+                     bar_s)
+                 : "memory");
+    for (int b = 0; b < NB; b++) {
+        const uint64_t ob = o + (uint64_t)b * BYTES;
+        if (ob >= nbytes) break;
+        const uint32_t sz = (uint32_t)(nbytes - ob < (uint64_t)BYTES ? nbytes - ob : BYTES);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(f(dst + ob)),
+                     "r"((uint32_t)__cvta_generic_to_shared(sm + b * BYTES)), "r"(sz)
+                     : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+template <int NB, int BYTES>
+int bulk_launch(F f, uint64_t dst, uint64_t src, uint64_t nvec, cudaStream_t s) {
+    const int smem = NB * BYTES + 16;
+    cudaFuncSetAttribute(v_bulk<NB, BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const uint64_t per = (uint64_t)NB * BYTES;
+    v_bulk<NB, BYTES><<<(unsigned)((nvec * 16 + per - 1) / per), 32, smem, s>>>(f, dst, src, nvec);
+    return 0;
+}
+
+extern "C" int variant_count() { return 18; }
 
 extern "C" const char *variant_name(int v) {
     static const char *n[] = {"persist U4 cs",   "persist U4 na",   "persist U4 def", "persist U8 cs",
                               "persist U8 na",   "chunk U4 cs",     "chunk U4 na",    "chunk U8 cs",
                               "chunk U8 na",     "pchunk U4 cs",    "pchunk U8 cs",   "pchunk U8 na",
-                              "persist U4 cs x2grid", "pchunk U16 na"};
+                              "persist U4 cs x2grid", "pchunk U16 na", "bulk 4x16K",     "bulk 2x16K",
+                              "bulk 4x8K",       "bulk 1x32K"};
     return n[v];
 }
 
@@ -145,6 +194,10 @@ extern "C" int variant_copy(int v, uint64_t base, uint64_t mask, uint64_t dst, u
         case 11: PERSIST((v_pchunk<8, 1>), 1); break;
         case 12: PERSIST((v_persist<4, 0>), 2); break;
         case 13: PERSIST((v_pchunk<16, 1>), 1); break;
+        case 14: bulk_launch<4, 16384>(f, dst, src, nvec, s); break;
+        case 15: bulk_launch<2, 16384>(f, dst, src, nvec, s); break;
+        case 16: bulk_launch<4, 8192>(f, dst, src, nvec, s); break;
+        case 17: bulk_launch<1, 32768>(f, dst, src, nvec, s); break;
     }
     return (int)cudaGetLastError();
 }
