@@ -123,6 +123,24 @@ def test_modulo_stencil_out_crossing_end(arenas, mode):
          None if mode == "modulo" else 6 * (W - 2))
 
 
+@pytest.mark.parametrize("mode", ["modulo", "check", "clamp"])
+def test_exact_partition_stencil_tma(arenas, mode):
+    """K5 v2 on an exact-size (non-power-of-two) partition: `in` far past the
+    end (modulo wraps the descriptor base, clamp moves it to the last legal
+    16-byte address, check refuses it) and `out` crossing the end."""
+    a, parts, rng = _setup(arenas, 607)
+    H, W, pitch = 120, 1001, 1004
+    p = parts[1]
+    inp = p.base + EXACT + 3 * MiB + 64                 # outside, 16-aligned
+    upload(p.base + 3 * MiB, synth.uniform_f32(rng, H * pitch, 0.0, 1.0))      # where modulo lands
+    upload(p.end - 4 * MiB, synth.uniform_f32(rng, MiB, 0.0, 1.0))
+    out = p.end - 60 * 4 * pitch - 4 * (W - 1)
+    _run(a, parts, 1, mode,
+         lambda p: a.stencil_tma(p.id, mode, out, inp, H, W, pitch, 0.5, 0.125),
+         lambda m, p: oracle.stencil_tma(m, p.base, p.size, mode, out, inp, H, W, pitch, 0.5, 0.125),
+         None if mode == "modulo" else H + (H - 1 - 61))
+
+
 @pytest.mark.parametrize("mode", ["modulo", "check"])
 def test_modulo_gemm_A_past_end(arenas, mode):
     a, parts, rng = _setup(arenas, 605)
