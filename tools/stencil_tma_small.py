@@ -1,6 +1,12 @@
-import sys, os
-sys.path.insert(0, "/root/repo")
-import torch
+"""Run one K5 v2 (TMA stencil) launch of the given H W pitch in mode none (dev tool, e.g. under compute-sanitizer).
+  python tools/stencil_tma_small.py H W pitch
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
 from paper_2401_09290_b200 import devmem, guardian as g
 MiB=1<<20
 a=g.Arena(0, 32*MiB); p=a.partition_alloc(16*MiB)
