@@ -159,3 +159,32 @@ def test_gemm_operand_in_victim(arenas, mode):
     _run(a, p, mode, p.base, victim.base + 4 * MiB, p.base + 8 * MiB, M, N, K, K, K, N,
          expect_viol=0 if mode == "mask" else N)
     assert np.array_equal(download(victim.base, victim.size), vb)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_gemm_fuzz(arenas, seed):
+    """Random ragged shapes (M any, N % 16, K % 64), padded strides and, in
+    the counting modes, A or C straddling the end or C below the base; both
+    1-SM (M < 256) and 2-SM paths."""
+    a, parts = _setup(arenas)
+    p = parts[seed % 2]
+    rng = synth.rng_for(420 + seed)
+    mode = ["none", "mask", "check", "modulo", "maskcount", "clamp"][seed % 6]
+    M = int(rng.integers(1, 600))
+    N = 16 * int(rng.integers(1, 40))
+    K = 64 * int(rng.integers(1, 9))
+    lda, ldb, ldc = K + 8 * int(rng.integers(0, 4)), K + 8 * int(rng.integers(0, 4)), N + 8 * int(rng.integers(0, 4))
+    A, B, C = p.base + 2 * MiB, p.base + 4 * MiB, p.base + 8 * MiB
+    if mode in ("check", "maskcount", "clamp"):
+        # one operand straddles the end or C lies below the base; operands
+        # never overlap (their fenced images stay disjoint too: race-free)
+        case = int(rng.integers(0, 3))
+        if case == 0:
+            A = p.end - 16 * int(rng.integers(1, (M * lda * 2) // 16 + 1))
+        elif case == 1:
+            C = p.end - 16 * int(rng.integers(1, (M * ldc * 2) // 16 + 1))
+        else:
+            C = p.base - 16 * int(rng.integers(1, 1 << 12))
+    upload(A, synth.bf16_bits_uniform(rng, min(M * lda, (p.end - A) // 2)))
+    upload(B, synth.bf16_bits_uniform(rng, N * ldb))
+    _run(a, p, mode, A, B, C, M, N, K, lda, ldb, ldc)
