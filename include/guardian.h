@@ -21,6 +21,11 @@
  *  - Asynchronous CUDA faults surface as GD_ERR_CUDA at the next synchronising
  *    call; gd_last_cuda_error() returns the cudaError_t behind GD_ERR_CUDA.
  *  - n = 0 launches are GD_OK and do nothing.
+ *  - Size limits (GD_ERR_INVALID_ARG beyond them; every grid stays below
+ *    2^31 CTAs): copy n <= 2^44 bytes; saxpy, scatter n <= 2^42 elements;
+ *    gather n * row_elems <= 2^42; stencil H * pitch <= 2^58 floats, and
+ *    the LSU stencil H <= 2^19 rows (GD_ERR_UNSUPPORTED; the TMA stencil has
+ *    no such limit).
  *  - Thread safety: arena mutations (partition alloc/free, malloc/free) are
  *    serialised by an internal mutex; launches read an immutable snapshot of
  *    the partition bounds entry and may be issued from several threads.

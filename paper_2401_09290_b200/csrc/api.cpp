@@ -505,13 +505,13 @@ gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool d
     switch (w.kind) {
         case GD_KIND_COPY:
             if ((w.ptr[0] | w.ptr[1]) % 16) return GD_ERR_ALIGN;
-            if (w.u64[0] > (1ull << 62)) return GD_ERR_INVALID_ARG;
+            if (w.u64[0] > (1ull << 44)) return GD_ERR_INVALID_ARG;      // grid < 2^31 CTAs
             bytes = 2 * w.u64[0];
             empty = w.u64[0] == 0;
             break;
         case GD_KIND_SAXPY:
             if ((w.ptr[0] | w.ptr[1]) % 16) return GD_ERR_ALIGN;
-            if (w.u64[0] > (1ull << 58)) return GD_ERR_INVALID_ARG;
+            if (w.u64[0] > (1ull << 42)) return GD_ERR_INVALID_ARG;
             bytes = 12 * w.u64[0];
             flops = 2 * w.u64[0];
             empty = w.u64[0] == 0;
@@ -519,13 +519,13 @@ gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool d
         case GD_KIND_GATHER:
             if ((w.ptr[0] | w.ptr[2]) % 16 || w.ptr[1] % 4) return GD_ERR_ALIGN;
             if (w.u32[0] == 0) return GD_ERR_INVALID_ARG;
-            if (!mul_ok(w.u64[0], (uint64_t)w.u32[0], &t) || t > (1ull << 58)) return GD_ERR_INVALID_ARG;
+            if (!mul_ok(w.u64[0], (uint64_t)w.u32[0], &t) || t > (1ull << 42)) return GD_ERR_INVALID_ARG;
             bytes = 4 * w.u64[0] + 8 * t;
             empty = w.u64[0] == 0;
             break;
         case GD_KIND_SCATTER:
             if ((w.ptr[1] | w.ptr[2]) % 16 || w.ptr[0] % 4) return GD_ERR_ALIGN;
-            if (w.u64[0] > (1ull << 58)) return GD_ERR_INVALID_ARG;
+            if (w.u64[0] > (1ull << 42)) return GD_ERR_INVALID_ARG;
             bytes = 16 * w.u64[0];
             empty = w.u64[0] == 0;
             break;
@@ -534,6 +534,7 @@ gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool d
             if ((w.ptr[0] | w.ptr[1]) % 16 || pitch % 4) return GD_ERR_ALIGN;
             if (pitch < W || !mul_ok(H, pitch, &t) || t > (1ull << 58)) return GD_ERR_INVALID_ARG;
             if (w.u32[2] > 1) return GD_ERR_INVALID_ARG;          // 0: K5 v1 (LSU), 1: K5 v2 (TMA)
+            if (w.u32[2] == 0 && H > (1ull << 19)) return GD_ERR_UNSUPPORTED;   // v1 grid.y <= 65535
             empty = H < 3 || W < 3;
             bytes = empty ? 0 : 8 * (H - 2) * (W - 2);
             flops = empty ? 0 : 5 * (H - 2) * (W - 2);

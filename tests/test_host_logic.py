@@ -203,6 +203,20 @@ def test_launch_validation_on_virtual_arena():
     with pytest.raises(g.GuardianError) as e:
         a.copy(p.id, "mask", p.base, p.base + 16, 64)                     # valid, but no device
     assert e.value.status == g.GD_ERR_UNSUPPORTED
+    # size limits (every grid below 2^31 CTAs), refused before anything runs
+    for call in (lambda: a.copy(p.id, "mask", p.base, p.base, (1 << 44) + 16),
+                 lambda: a.saxpy(p.id, "mask", 1.0, p.base, p.base, (1 << 42) + 4),
+                 lambda: a.gather(p.id, "mask", p.base, p.base, p.base, (1 << 40) + 4, 8),
+                 lambda: a.scatter(p.id, "mask", p.base, p.base, p.base, (1 << 42) + 4)):
+        with pytest.raises(g.GuardianError) as e:
+            call()
+        assert e.value.status == g.GD_ERR_INVALID_ARG
+    with pytest.raises(g.GuardianError) as e:
+        a.stencil(p.id, "mask", p.base, p.base, (1 << 19) + 1, 8, 8, 0.5, 0.125)
+    assert e.value.status == g.GD_ERR_UNSUPPORTED
+    with pytest.raises(g.GuardianError) as e:                          # the TMA stencil takes it
+        a.stencil_tma(p.id, "mask", p.base, p.base, (1 << 19) + 1, 8, 8, 0.5, 0.125)
+    assert e.value.status == g.GD_ERR_UNSUPPORTED                         # (valid; no device here)
 
 
 def test_arena_wrap_errors():
