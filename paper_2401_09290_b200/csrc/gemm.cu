@@ -50,10 +50,12 @@ constexpr uint32_t EPI_BYTES = 4 * 2 * EPI_CHUNK_BYTES;        // 4 epilogue war
 constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int THREADS = 256;
 constexpr uint32_t TMEM_COLS = ACC * BN;           // 512
-// raster group (m-blocks): probe (tools/gemm_group_probe.sh) at 8192^3 -- DRAM
-// reads 1.52 / 1.10 / 1.25 / 2.27 GB for groups 4 / 8 / 16 / 32, and under the
-// 1 kW power cap sustained TFLOP/s follow the DRAM traffic (8 is best)
-constexpr uint32_t GROUP_M = 16;   // raster group (m-blocks); probe: profiles/r01_gemm_krev_probe.txt
+// raster group (m-blocks).  With forward-only K loops, groups 4 / 8 / 16 / 32
+// read 1.52 / 1.10 / 1.25 / 2.27 GB per 8192^3 launch (8 best,
+// profiles/r01_gemm_group_probe.txt); with K-alternating waves (krev) a group
+// of 16 reads 0.92 GB and runs fastest (profiles/r01_gemm_krev_probe.txt).
+// Under the 1 kW power cap sustained TFLOP/s follow the DRAM traffic.
+constexpr uint32_t GROUP_M = 16;
 
 // instruction descriptor: D f32, A/B bf16, both K-major, N=256, M=128
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
