@@ -9,9 +9,9 @@
 // D = 1 path: each CTA owns a contiguous chunk of kThreads x kU index
 // vectors; per thread kU 128-bit index loads, then 4 kU independent fenced
 // random 32-bit table loads (L1-bypassing, sector-granular), then kU 128-bit
-// output stores.  In check mode the index and output streams are range-tested
-// once per CTA chunk (fence.cuh range_in); the random table accesses are
-// checked one by one.  D % 4 == 0 with 16-byte-aligned table and output:
+// output stores.  In the hoistable modes (check, modulo, mask-count, clamp)
+// the index and output streams are range-tested once per CTA chunk (fence.cuh
+// range_in); the random table accesses are fenced one by one.  D % 4 == 0 with 16-byte-aligned table and output:
 // row slots of 128-bit vectors (k_gatherR below).  Other D > 1: one warp per
 // index row, lanes stride over the row; lane 0 loads the index once (one
 // logical access, as in the oracle) and broadcasts it.

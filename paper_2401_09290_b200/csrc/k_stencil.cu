@@ -12,10 +12,11 @@
 // is fenced at its own width; the values a point uses are exactly the values
 // its five logical loads would read (a 16-byte-aligned vector is wholly
 // inside or wholly outside a pow2 partition, and F(a+4k,4) = F(a,16)+4k).
-// Check-mode refusals are counted per logical access: 5 loads + 1 store per
-// interior point, as in the oracle.  Check mode hoists one conservative range
-// test per thread strip (fence.cuh range_in): strips wholly inside the
-// partition run the unchecked body, the rest the per-access checked body.
+// Refusals / detections are counted per logical access: 5 loads + 1 store per
+// interior point, as in the oracle.  The hoistable modes (check, modulo,
+// mask-count, clamp) take one conservative range test per thread strip
+// (fence.cuh range_in): strips wholly inside the partition run the unfenced
+// body, the rest the per-access fenced body.
 #include "fence.cuh"
 #include "kernels.h"
 
