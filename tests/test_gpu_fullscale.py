@@ -48,7 +48,7 @@ def _c3_inputs(a, p, seed, frac):
     return idx, pos
 
 
-@pytest.mark.parametrize("mode", ["mask", "check"])
+@pytest.mark.parametrize("mode", ["mask", "check", "maskcount", "clamp"])
 def test_c3_gather_full(two_tenants, mode):
     a, victim, p = two_tenants
     gen = torch.Generator(device="cuda:0")
@@ -74,8 +74,11 @@ def test_c3_gather_full(two_tenants, mode):
     if mode == "check":
         assert st["violations"] == 671089
         assert (out[pos_t] == 0).all()
+    elif mode == "clamp":                        # every planted j < 0 lands below the base: word 0
+        assert st["violations"] == 671089
+        assert (out[pos_t] == table[0]).all()
     else:
-        assert st["violations"] == 0
+        assert st["violations"] == (671089 if mode == "maskcount" else 0)
         j = idx[pos].astype(np.int64)
         expect = synth.pattern_words(np.mod(PART + 4 * j, PART).astype(np.uint64)).view(np.int32)
         np.testing.assert_array_equal(out[pos_t].cpu().numpy(), expect)
