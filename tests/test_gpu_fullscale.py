@@ -94,7 +94,7 @@ def test_c3_gather_full(two_tenants, mode):
         assert outs[i] == want, (i, idx[i], outs[i], want)
 
 
-@pytest.mark.parametrize("mode", ["mask", "check"])
+@pytest.mark.parametrize("mode", ["mask", "check", "maskcount", "clamp"])
 def test_c3_scatter_full(two_tenants, mode):
     a, victim, p = two_tenants
     idx, pos = _c3_inputs(a, p, 3002, 0.01)
@@ -102,7 +102,7 @@ def test_c3_scatter_full(two_tenants, mode):
     a.stats_reset()
     a.scatter(p.id, mode, p.base, p.base + IDX_OFF, p.base + OUT_OFF, N_IDX)
     st = a.stats(p.id)
-    assert st["violations"] == (671089 if mode == "check" else 0)
+    assert st["violations"] == (0 if mode == "mask" else 671089)
     after = devmem.view(p.base, PART // 4, torch.int32)
     src = devmem.view(p.base + OUT_OFF, N_IDX, torch.int32).long() & 0xFFFFFFFF
     idx_t = torch.from_numpy(idx.astype(np.int64)).cuda()
@@ -112,9 +112,11 @@ def test_c3_scatter_full(two_tenants, mode):
     # table region: index_add_ reference (int64, reduced mod 2^32)
     ref = before[:T_N].long() & 0xFFFFFFFF
     ref.index_add_(0, idx_t[inb], src[inb])
+    if mode == "clamp":                          # every planted j < 0 clamps to word 0 (sums per CTA, exact)
+        ref[0] += src[pos_t].sum()
     assert torch.equal(after[:T_N].long() & 0xFFFFFFFF, ref & 0xFFFFFFFF)
     del ref
-    if mode == "mask":
+    if mode in ("mask", "maskcount"):
         # planted indices: the oracle fences each raw address; the adds land there
         raw = (p.base + 4 * idx[pos].astype(np.int64)).astype(np.uint64)
         f = oracle.fence_mask_n(raw, p.base, p.size, 4)
