@@ -12,7 +12,15 @@
  *     (§4.2.3, §4.4); an access that fails the
  *     check is not performed (loads read 0, stores are dropped) and is
  *     counted.
+ *   - modulo: partition_base + ((addr - partition_base) % partition_size)
+ *     (§4.4; u64 remainder, reading A10).
+ *   - mask-count / clamp: the mask fence plus detection (SURVEY.md §8(c)
+ *     A14) / north_star's "compare, clamp and set a violation flag" (A1):
+ *     both count exactly the accesses check mode refuses.
  *   - none: the native kernel.
+ *   - descriptor-fenced operands (TMA kernels, §8(c) O2): the operand base is
+ *     fenced like a 16-byte access and its row count clamped to the
+ *     partition (or_desc_rows; or_gemm, or_stencil_tma).
  */
 #include "oracle.h"
 
