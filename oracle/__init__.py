@@ -14,6 +14,7 @@ partition allocator used to check the product allocator's invariants
 from __future__ import annotations
 
 import ctypes
+import threading
 import os
 from dataclasses import dataclass
 
@@ -52,16 +53,23 @@ def build(force: bool = False) -> str:
             and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(src), os.path.getmtime(hdr))):
         return LIB_PATH
     import subprocess
-    tmp = LIB_PATH + ".tmp"
+    tmp = f"{LIB_PATH}.{os.getpid()}.tmp"           # unique: concurrent builders never collide
     subprocess.check_call(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math",
                            "-fPIC", "-shared", "-Wall", "-Wextra", "-o", tmp, src, "-lm"])
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
 
+_lib_lock = threading.Lock()
+
+
 def lib():
     global _lib
-    if _lib is None:
+    if _lib is not None:
+        return _lib
+    with _lib_lock:                      # threads of one process: build and load once
+        if _lib is not None:
+            return _lib
         build()
         L = ctypes.CDLL(LIB_PATH)
         u64, u32, f32, i32 = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_float, ctypes.c_int
