@@ -57,6 +57,20 @@ struct Fence {
             return a;
         }
     }
+    // MODULO, strength-reduced along a walk known not to wrap (every address
+    // of the walk on one side of base, so the u64 offsets a - base do not
+    // cross 2^64 (A10), and d < size): the fence of a_prev + d / of
+    // a_next - d from the fence of a_prev / a_next, one add and one select,
+    // equal to addr() (the residues stay W-aligned when base, the addresses,
+    // d and size are).
+    __device__ __forceinline__ uint64_t step_up(uint64_t f_prev, uint64_t d) const {
+        const uint64_t r = (f_prev - base) + d;
+        return base + (r >= size ? r - size : r);
+    }
+    __device__ __forceinline__ uint64_t step_down(uint64_t f_next, uint64_t d) const {
+        const uint64_t r = f_next - base;
+        return base + (r >= d ? r - d : r + (size - d));
+    }
     // the check predicate: every byte in the partition, a W-aligned
     __device__ __forceinline__ bool inside(uint64_t a) const {
         return (a - base) <= lim && (a & (uint64_t)(W - 1)) == 0;

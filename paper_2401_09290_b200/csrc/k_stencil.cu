@@ -13,10 +13,12 @@
 // its five logical loads would read (a 16-byte-aligned vector is wholly
 // inside or wholly outside a pow2 partition, and F(a+4k,4) = F(a,16)+4k).
 // Refusals / detections are counted per logical access: 5 loads + 1 store per
-// interior point, as in the oracle.  The hoistable modes (check, modulo,
-// mask-count, clamp) take one conservative range test per thread strip
-// (fence.cuh range_in): strips wholly inside the partition run the unfenced
-// body, the rest the per-access fenced body.
+// interior point, as in the oracle, each when its load is issued (with the
+// number of strip points that use the loaded vector).  The hoistable modes
+// (check, modulo, mask-count, clamp) take one conservative range test per
+// thread strip (fence.cuh range_in): strips wholly inside the partition run
+// the unfenced body, the rest the per-access fenced body.  With hoisting off
+// (GD_CHECK_PER_ACCESS=1) k_stencil_pa fences every access of every strip.
 #include "fence.cuh"
 #include "kernels.h"
 
@@ -29,9 +31,10 @@ constexpr int kRows = 16;     // rows per CTA strip (a multiple of the rows load
 __device__ __forceinline__ void st_v(uint64_t a, uint4 v) { __stcs(reinterpret_cast<uint4 *>(a), v); }
 __device__ __forceinline__ void st_w(uint64_t a, uint32_t v) { __stcs(reinterpret_cast<unsigned int *>(a), v); }
 
-template <int MODE, int kG>
+template <int MODE, int kG, bool WALK = false>
 __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t W, uint64_t pitch,
-                                      float c0, float c1, uint64_t c, uint64_t r0, uint64_t r1, uint32_t &nv) {
+                                      float c0, float c1, uint64_t c, uint32_t r0, uint32_t r1, uint32_t &nv) {
+    // row indices are 32-bit (H <= 2^19, api.cpp); addresses are 64-bit
     const Fence<MODE, 16> f16(fd);
     const Fence<MODE, 4> f4(fd);
     bool interior[4];
@@ -41,60 +44,89 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         interior[k] = (c + k >= 1) && (c + k + 2 <= W);
         all4 = all4 && interior[k];
     }
-    // refused-access weights (check mode): loads of the own vector used by
-    // the interior points as C (each), as W (k >= 1) and as E (k <= 2)
+    // refused-access weights (counting modes): the own vector of row x is
+    // loaded by the interior points of row x as C (each), as W (k >= 1) and
+    // as E (k <= 2), and by those of rows x-1 / x+1 as S / N (once each).
+    // A refusal is counted when the vector is loaded, with the weight of the
+    // strip rows [r0, r1) that use it, so no per-load flag stays live.
     uint32_t ni = 0, nCv = 0;
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         ni += interior[k];
         nCv += interior[k] * (1u + (k >= 1) + (k <= 2));
     }
-    // ok = the vector's / word's accesses are not counted (check: performed);
+    auto weight = [&](uint32_t x) {
+        return ni * ((uint32_t)(x >= r0 + 1 && x <= r1) + (uint32_t)(x + 1 >= r0 && x + 1 < r1)) +
+               nCv * (uint32_t)(x >= r0 && x < r1);
+    };
+    // modulo with WALK (the strip does not straddle the base and a row step
+    // is below the partition size): the rows are loaded in increasing order,
+    // so each vector's fence follows from the previous row's
+    // (Fence::step_up), the W / E words of a row from the fence of the row
+    // below it (step_down) and each output vector from the previous output
+    // row's; every access still gets its own fenced address, equal to the
+    // full modulo.  Without WALK every access takes the full modulo.
+    uint64_t f_last = 0, fo_last = 0;
     // a clamped outside vector is its edge word four times (fence.cuh vld4)
-    auto ldv = [&](uint64_t r, bool &ok) {
-        const uint64_t a = in + 4 * (r * pitch + c);
-        ok = counts(MODE) ? f16.inside(a) : true;
+    auto ldv = [&](uint32_t r) {
+        const uint64_t a = in + 4 * ((uint64_t)r * pitch + c);
+        if constexpr (MODE == kModulo && WALK) {
+            f_last = r == r0 - 1 ? f16.addr(a) : f16.step_up(f_last, 4 * pitch);
+            return __ldg(reinterpret_cast<const float4 *>(f_last));
+        }
+        const bool ok = counts(MODE) ? (a - f16.base) <= f16.lim : true;    // a is 16-aligned (API)
+        if constexpr (counts(MODE)) nv += ok ? 0u : weight(r);
         if constexpr (MODE == kClamp) {
             if (ok) return __ldg(reinterpret_cast<const float4 *>(a));
             const float w = __ldg(reinterpret_cast<const float *>(f16.edge4(a)));
             return make_float4(w, w, w, w);
+        } else if constexpr (MODE == kCheck) {
+            // predicated: the destination is zeroed before the load, so
+            // nothing consumes the loaded value until the stencil uses it
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ok) v = __ldg(reinterpret_cast<const float4 *>(a));
+            return v;
         } else {
-            return f16.ok(a) ? __ldg(reinterpret_cast<const float4 *>(f16.addr(a))) : make_float4(0.f, 0.f, 0.f, 0.f);
+            return __ldg(reinterpret_cast<const float4 *>(f16.addr(a)));
         }
     };
-    auto lds = [&](uint64_t e, bool &ok) {
+    auto lds = [&](uint64_t e, uint64_t a_below) {     // one logical access of one point
         const uint64_t a = in + 4 * e;
-        ok = counts(MODE) ? f4.inside(a) : true;
-        return f4.ok(a) ? __ldg(reinterpret_cast<const float *>(f4.addr(a))) : 0.f;
+        if constexpr (MODE == kModulo && WALK) {       // f_last: the fence of the vector of the row below
+            return __ldg(reinterpret_cast<const float *>(f4.step_down(f_last, a_below - a)));
+        }
+        const bool ok = counts(MODE) ? (a - f4.base) <= f4.lim : true;      // a is 4-aligned
+        if constexpr (counts(MODE)) nv += ok ? 0u : 1u;
+        if constexpr (MODE == kCheck) {
+            float v = 0.f;
+            if (ok) v = __ldg(reinterpret_cast<const float *>(a));
+            return v;
+        } else {
+            return __ldg(reinterpret_cast<const float *>(f4.addr(a)));
+        }
     };
-    bool okP, okC;
-    float4 P = ldv(r0 - 1, okP);
-    float4 Cv = ldv(r0, okC);
-    for (uint64_t r = r0; r < r1; r += kG) {
+    float4 P = ldv(r0 - 1);
+    float4 Cv = ldv(r0);
+    for (uint32_t r = r0; r < r1; r += kG) {
         float4 S[kG];
-        bool okS[kG];
         float wv[kG], ev[kG];
-        bool okW[kG], okE[kG];
 #pragma unroll
         for (int g = 0; g < kG; g++) {
-            const uint64_t rr = r + g;
-            okS[g] = okW[g] = okE[g] = true;
+            const uint32_t rr = r + g;
             S[g] = make_float4(0.f, 0.f, 0.f, 0.f);
             wv[g] = ev[g] = 0.f;
             if (rr < r1) {
-                S[g] = ldv(rr + 1, okS[g]);
-                if (interior[0]) wv[g] = lds(rr * pitch + c - 1, okW[g]);
-                if (interior[3]) ev[g] = lds(rr * pitch + c + 4, okE[g]);
+                S[g] = ldv(rr + 1);
+                if (interior[0]) wv[g] = lds((uint64_t)rr * pitch + c - 1, in + 4 * ((uint64_t)(rr + 1) * pitch + c));
+                if (interior[3]) ev[g] = lds((uint64_t)rr * pitch + c + 4, in + 4 * ((uint64_t)(rr + 1) * pitch + c));
             }
         }
 #pragma unroll
         for (int g = 0; g < kG; g++) {
-            const uint64_t rr = r + g;
+            const uint32_t rr = r + g;
             if (rr < r1) {
                 const float4 N = (g == 0) ? P : ((g == 1) ? Cv : S[g >= 2 ? g - 2 : 0]);
                 const float4 C = (g == 0) ? Cv : S[g >= 1 ? g - 1 : 0];
-                const bool okN = (g == 0) ? okP : ((g == 1) ? okC : okS[g >= 2 ? g - 2 : 0]);
-                const bool okCC = (g == 0) ? okC : okS[g >= 1 ? g - 1 : 0];
                 const float cn[4] = {N.x, N.y, N.z, N.w};
                 const float cc[4] = {C.x, C.y, C.z, C.w};
                 const float cs[4] = {S[g].x, S[g].y, S[g].z, S[g].w};
@@ -108,14 +140,19 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
                     const float s = __fadd_rn(ns, we);
                     o[k] = __fmaf_rn(c1, s, __fmul_rn(c0, cc[k]));
                 }
-                if constexpr (counts(MODE)) {
-                    // per interior point: N, S, C loads; W from the own vector
-                    // unless k == 0; E from the own vector unless k == 3
-                    nv += ni * ((uint32_t)!okN + (uint32_t)!okS[g]) + nCv * (uint32_t)!okCC +
-                          (uint32_t)!okW[g] + (uint32_t)!okE[g];
-                }
-                const uint64_t ao = out + 4 * (rr * pitch + c);
-                if (all4) {
+                const uint64_t ao = out + 4 * ((uint64_t)rr * pitch + c);
+                if constexpr (MODE == kModulo && WALK) {
+                    // F4(ao + 4k) = F16(ao) + 4k
+                    fo_last = rr == r0 ? f16.addr(ao) : f16.step_up(fo_last, 4 * pitch);
+                    if (all4) {
+                        st_v(fo_last, make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
+                                                 __float_as_uint(o[3])));
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 4; k++)
+                            if (interior[k]) *reinterpret_cast<float *>(fo_last + 4 * k) = o[k];
+                    }
+                } else if (all4) {
                     vst4(f16, ao,
                          make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
                                     __float_as_uint(o[3])),
@@ -131,15 +168,9 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
             }
         }
         // slide the window: rows r+kG-1 (new P) and r+kG (new C)
-        if constexpr (kG >= 2) {
-            P = S[kG - 2];
-            okP = okS[kG - 2];
-        } else {
-            P = Cv;
-            okP = okC;
-        }
+        if constexpr (kG >= 2) P = S[kG - 2];
+        else P = Cv;
         Cv = S[kG - 1];
-        okC = okS[kG - 1];
     }
 }
 
@@ -153,11 +184,10 @@ template <int MODE, int ROWS>
 __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                          uint64_t in, uint32_t H, uint32_t W, uint64_t pitch,
                                                          float c0, float c1) {
-    constexpr uint64_t rows = ROWS;
     uint32_t nv = 0;
     const uint64_t c = 4ull * ((uint64_t)blockIdx.x * kThreads + threadIdx.x);
-    const uint64_t r0 = 1ull + (uint64_t)blockIdx.y * rows;
-    const uint64_t r1 = (r0 + rows < (uint64_t)H - 1) ? r0 + rows : (uint64_t)H - 1;
+    const uint32_t r0 = 1u + blockIdx.y * (uint32_t)ROWS;
+    const uint32_t r1 = (r0 + ROWS < H - 1) ? r0 + ROWS : H - 1;
     if (c < W && r0 < r1) {
         if constexpr (hoistable(MODE)) {
             // conservative extents of everything this strip touches; inside the
@@ -177,17 +207,53 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__
     if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }
 
+// Per-access fencing (fd.flags & kNoHoist, GD_CHECK_PER_ACCESS=1, the
+// paper's instrumentation): no range test, every strip runs the fenced body
+// with 4 rows of loads in flight, inside 64 registers in every mode (the
+// hoisted kernel's edge body keeps one row in flight next to its unfenced
+// body).
+template <int MODE, int ROWS>
+__global__ void __launch_bounds__(kThreads, 4) k_stencil_pa(const __grid_constant__ FenceDesc fd, uint64_t out,
+                                                            uint64_t in, uint32_t H, uint32_t W, uint64_t pitch,
+                                                            float c0, float c1) {
+    uint32_t nv = 0;
+    const uint64_t c = 4ull * ((uint64_t)blockIdx.x * kThreads + threadIdx.x);
+    const uint32_t r0 = 1u + blockIdx.y * (uint32_t)ROWS;
+    const uint32_t r1 = (r0 + ROWS < H - 1) ? r0 + ROWS : H - 1;
+    if (c < W && r0 < r1) {
+        if constexpr (MODE == kModulo) {
+            // the walk recurrence holds when no operand range of the strip
+            // straddles the base (the u64 offsets do not wrap) and a row step
+            // is below the partition size
+            const uint64_t lo_in = in + 4 * ((r0 - 1) * pitch + c) - (c ? 4 : 0);
+            const uint64_t hi_in = in + 4 * (r1 * pitch + c + 5);
+            const uint64_t lo_out = out + 4 * (r0 * pitch + c), hi_out = out + 4 * ((r1 - 1) * pitch + c + 4);
+            const auto side = [&](uint64_t lo, uint64_t hi) { return lo <= hi && (hi <= fd.base || lo >= fd.base); };
+            if (4 * pitch < fd.size && side(lo_in, hi_in) && side(lo_out, hi_out))
+                strip<MODE, 4, true>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+            else
+                strip<MODE, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+        } else {
+            strip<MODE, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+        }
+    }
+    if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
+}
+
 template <int MODE>
 cudaError_t stencil_t(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t H, uint32_t W, uint64_t pitch,
                       float c0, float c1, cudaStream_t s, int sms) {
     const uint64_t nvec = (W + 3ull) / 4, gx = (nvec + kThreads - 1) / kThreads;
     // long strips unless that leaves fewer than 4 CTAs per SM
+    const bool pa = hoistable(MODE) && (fd.flags & kNoHoist);
     if (gx * ((H - 2ull + kRows - 1) / kRows) >= 4ull * (uint64_t)sms) {
         const dim3 grid((unsigned)gx, (unsigned)((H - 2ull + kRows - 1) / kRows));
-        k_stencil<MODE, kRows><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
+        if (pa) k_stencil_pa<MODE, kRows><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
+        else k_stencil<MODE, kRows><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
     } else {
         const dim3 grid((unsigned)gx, (unsigned)((H - 2ull + 7) / 8));
-        k_stencil<MODE, 8><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
+        if (pa) k_stencil_pa<MODE, 8><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
+        else k_stencil<MODE, 8><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
     }
     return cudaGetLastError();
 }

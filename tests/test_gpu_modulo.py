@@ -124,6 +124,38 @@ def test_modulo_stencil_out_crossing_end(arenas, mode):
 
 
 @pytest.mark.parametrize("mode", ["modulo", "check", "clamp"])
+@pytest.mark.parametrize("case", ["in_crossing_end", "in_below_base", "pitch_past_size"])
+def test_modulo_stencil_walk(arenas, mode, case):
+    """The per-access stencil's modulo fence follows each row's vector from
+    the row before (Fence::step_up), the W / E words from the row below
+    (step_down) and each output row from the one before, when the strip does
+    not straddle the base and a row step is below the partition size; other
+    strips take the full modulo per access.  Every path against the oracle's
+    plain u64 remainder: the walk stepping over the partition end
+    (conditional subtract), `in` starting below the base (strips wholly
+    below it walk on wrapped offsets, the straddling strip takes the full
+    modulo), and a row step of more than the partition size (full modulo).
+    Run hoisted here and per access by test_gpu_peraccess.py."""
+    a, parts, rng = _setup(arenas, 605)
+    p = parts[1]
+    # finite values everywhere a wrapped row can land (random bytes hold NaNs,
+    # whose payloads the GPU and the host propagate differently)
+    upload(p.base, synth.uniform_f32(rng, p.size // 4, 0.0, 1.0))
+    if case == "pitch_past_size":
+        if mode == "clamp":
+            pytest.skip("the output row lies past the end: its clamped stores collide (reading R-race)")
+        H, W, pitch = 3, 200, EXACT // 4 + 4096
+        inp = p.base + 4 * MiB
+    else:
+        H, W, pitch = 160, 1000, 1024
+        inp = p.end - 40 * pitch * 4 if case == "in_crossing_end" else p.base - 40 * pitch * 4 - 64
+    out = p.base + 1 * MiB
+    _run(a, parts, 1, mode,
+         lambda p: a.stencil(p.id, mode, out, inp, H, W, pitch, 0.5, 0.125),
+         lambda m, p: oracle.stencil(m, p.base, p.size, mode, out, inp, H, W, pitch, 0.5, 0.125))
+
+
+@pytest.mark.parametrize("mode", ["modulo", "check", "clamp"])
 def test_exact_partition_stencil_tma(arenas, mode):
     """K5 v2 on an exact-size (non-power-of-two) partition: `in` far past the
     end (modulo wraps the descriptor base, clamp moves it to the last legal

@@ -73,19 +73,31 @@ def time_modes(launch, reps, warm=3, extra=None):
 
 def time_modes_batched(launch, reps, batch=50, warm=3):
     """L2-resident regime: kernels of a few microseconds are timed as a batch
-    of back-to-back launches between two events (per-launch mean)."""
+    of back-to-back launches between two events (per-launch mean).  Each
+    mode's batch is captured once into a CUDA graph and replayed, so the
+    host cost of a launch through the binding (several microseconds of
+    Python + C ABI) cannot hide the kernel time."""
     s = torch.cuda.Stream()
     res = {m: [] for m in MODES}
+    graphs = {}
     with torch.cuda.stream(s):
         for m in res:
             for _ in range(warm):
                 launch(m, s)
+        s.synchronize()
+        for m in res:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=s):
+                for _ in range(batch):
+                    launch(m, s)
+            graphs[m] = gr
+        for m in res:
+            graphs[m].replay()
         for _ in range(reps):
             for m in res:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(s)
-                for _ in range(batch):
-                    launch(m, s)
+                graphs[m].replay()
                 b.record(s)
                 b.synchronize()
                 res[m].append(a.elapsed_time(b) / batch)
@@ -97,10 +109,11 @@ def summarize(name, res, work, unit, peak):
     for m, xs in res.items():
         med = statistics.median(xs)
         rate = work / (med / 1e3) / (1e9 if unit == "GB/s" else 1e12)
-        out[m] = {"ms_median": round(med, 4), "ms_paper_mean": round(paper_mean(xs), 4), unit: round(rate, 1),
+        out[m] = {"ms_median": round(med, 6), "ms_paper_mean": round(paper_mean(xs), 6), unit: round(rate, 1),
                   "frac_of_peak": round(rate / peak, 4)}
+    base = statistics.median(res["none"])
     for m in (m for m in MODES if m != "none"):
-        out[m]["overhead_pct"] = round(100 * (out[m]["ms_median"] / out["none"]["ms_median"] - 1), 2)
+        out[m]["overhead_pct"] = round(100 * (statistics.median(res[m]) / base - 1), 2)
     print(f"{name:28s} " + "  ".join(f"{m}: {out[m][unit]:8.1f} {unit}" + (f" ({out[m]['overhead_pct']:+.2f}%)"
                                                                            if m != 'none' else '')
                                      for m in out), file=sys.stderr)
