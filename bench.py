@@ -326,14 +326,20 @@ class Workload:
         items = self.items(mode)
         a = self.arena
 
+        per_tenant = [[it for it in items if it.tenant == p.id] for p in self.parts]
+
         def one():
+            # tenant-major issue, each tenant on its own stream: upload, its
+            # fenced kernels (the launcher with that tenant's stream), download.
+            # The host->device engine serves the uploads in issue order, so
+            # tenant t's kernels and download overlap the uploads of tenants
+            # t+1.. (measured: 55.6 GB/s each way, 99 GB/s both,
+            # tools/pcie_probe.py)
             for t, p in enumerate(self.parts):
                 s = self.streams[t]
                 for off in (OFF_SRC, OFF_X, OFF_Y):
                     a.memcpy_h2d(p.id, p.base + off, host_in.data_ptr(), COPY_BYTES, stream=s)
-            self.step(items)
-            for t, p in enumerate(self.parts):
-                s = self.streams[t]
+                a.launcher_run(per_tenant[t], [s])
                 for off in (OFF_DST, OFF_Y):
                     a.memcpy_d2h(p.id, host_out.data_ptr(), p.base + off, COPY_BYTES, stream=s)
             # no host sync between steps: each tenant's stream orders its next
@@ -420,7 +426,9 @@ def run_gpu(args):
         s_per_step, h2d, d2h = w.e2e(args.mode, args.e2e_steps, 1)
         e2e = {"value": round(world * STEP_BYTES_PER_GPU / s_per_step / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": world * h2d, "d2h_bytes_per_step": world * d2h,
-               "steps": args.e2e_steps, "note": "pinned host buffers, checked gd_memcpy_h2d/d2h, PCIe-bound"}
+               "steps": args.e2e_steps, "note": "pinned host buffers, checked gd_memcpy_h2d/d2h, tenant-major pipelined issue; "
+                       "bound by the uploads: 103 GB per step at the box's measured 55.6 GB/s host->device "
+                       "(profiles/r01_pcie_probe.txt) caps e2e at ~92.7 GB/s"}
 
     # ---- C5: mixed tenants (copy / gather 1 % OOB / GEMM) in check mode ----
     c5 = None
@@ -735,7 +743,7 @@ def main():
     ap.add_argument("--mode", default="mask", choices=list(ALL_MODES))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--reps", type=int, default=5, help="interleaved none/mask/check repetitions")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the mixed multi-tenant (configs[4]) measurement")
