@@ -111,11 +111,37 @@ class Clocks:
 # distributed plumbing
 # ---------------------------------------------------------------------------
 
+_JSON_FD = None
+
+
+def quiet_stdout():
+    """Route everything written to fd 1 (NCCL prints "NCCL version ..." to
+    stdout at communicator setup) to stderr; emit() writes the one JSON line
+    to the original stdout."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line):
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        sys.stdout.flush()
+        os.write(_JSON_FD, data)
+
+
 def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    # GD_FORCE_DIST=1 brings NCCL up at world size 1 too, so a one-GPU box
+    # exercises the collective path (stats all_reduce, max-over-ranks timing)
+    if world > 1 or os.environ.get("GD_FORCE_DIST") == "1":
         import torch.distributed as dist
         import torch
         torch.cuda.set_device(local)
@@ -498,7 +524,7 @@ def run_gpu(args):
             "kernels_all_modes": table,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     w.arena.close()
 
 
@@ -756,7 +782,11 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     else:
+        quiet_stdout()
         run_gpu(args)
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":

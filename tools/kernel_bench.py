@@ -238,6 +238,11 @@ def main():
         r = time_modes_batched(lambda m, s: arena.stencil(p.id, m, b + 448 * MiB, b + 384 * MiB, H, W, W, 0.5, 0.125,
                                                           stream=s), args.reps)
         results["l2_stencil_2048^2"] = summarize("L2 stencil 2048^2", r, 8 * (H - 2) * (W - 2), "GB/s", hbm)
+        # K5 v2 at the same L2-resident size: the fence lives in the tensor maps
+        r = time_modes_batched(lambda m, s: arena.stencil_tma(p.id, m, b + 448 * MiB, b + 384 * MiB, H, W, W, 0.5,
+                                                              0.125, stream=s), args.reps)
+        results["l2_stencil_tma_2048^2"] = summarize("L2 stencil v2 (TMA) 2048^2", r, 8 * (H - 2) * (W - 2), "GB/s",
+                                                     hbm)
 
     if want("gemm"):
         n = 8192
