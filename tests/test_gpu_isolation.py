@@ -56,16 +56,26 @@ def test_no_foreign_reads(arenas, mode):
             assert np.array_equal(download(q.base, q.size), snaps[t]), f"partition {t} modified"
 
 
-def _sanitize(mode):
+def _sanitize(mode, env=None):
     exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     cmd = [exe, "--tool", "memcheck", "--error-exitcode", "9", sys.executable,
            os.path.join(ROOT, "tools", "adversarial.py"), "--mode", mode]
-    return subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                          env=dict(os.environ, **(env or {})))
 
 
 @pytest.mark.parametrize("mode", ["mask", "modulo", "check", "maskcount", "clamp"])
 def test_sanitizer_clean_when_fenced(mode):
     r = _sanitize(mode)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("mode", ["modulo", "check", "maskcount", "clamp"])
+def test_sanitizer_clean_per_access(mode):
+    """The per-access kernels (GD_CHECK_PER_ACCESS=1: no tile-level range
+    test, k_stencil_pa, the modulo row walk) on the same adversarial run."""
+    r = _sanitize(mode, {"GD_CHECK_PER_ACCESS": "1"})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr
 
