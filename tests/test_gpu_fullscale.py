@@ -179,6 +179,45 @@ def test_c4_stencil_full_sampled_rows(arenas):
         np.testing.assert_array_equal(got, want, err_msg=f"row {r}")
 
 
+@pytest.mark.parametrize("mode", ["mask", "check", "modulo", "maskcount"])
+def test_c4_stencil_full_out_crossing_end(arenas, mode):
+    """SURVEY.md §8(d) C4 adversarial layout at the bench size: `out` at
+    end - (H-64)·pitch·4, so its last 64 rows lie past the end.  Mask /
+    modulo wrap them into offsets [0, 64·pitch·4) (untouched otherwise, so
+    the run is race-free); check refuses and counts their 63·(W-2) interior
+    stores; mask-count stores like mask and counts like check.  Sampled rows
+    (inside, the first crossing row, the last) against the oracle's 3-row
+    band.  Run hoisted here and per access (k_stencil_pa, the modulo walk)
+    by test_gpu_peraccess.py."""
+    a = arenas(PART)
+    p = a.partition_alloc(PART)
+    H = W = 32768
+    inp, out = p.base + 4 * GiB, p.end - (H - 64) * W * 4
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(4001)
+    devmem.view(inp, H * W, torch.float32).uniform_(0, 1, generator=gen)
+    a.stats_reset()
+    a.stencil(p.id, mode, out, inp, H, W, W, 0.5, 0.125)
+    v = a.stats(p.id)["violations"]
+    assert v == (63 * (W - 2) if mode in ("check", "maskcount") else 0)
+    rows = [1, 2, 1000, H - 66, H - 65, H - 64, H - 63, H - 3, H - 2]
+    for r in rows:
+        band = download(inp + 4 * (r - 1) * W, 3 * 4 * W)
+        m = oracle.Mem(0x20000000, 4 << 20)
+        m.buf[:band.size] = band
+        oracle.stencil(m, 0x20000000, 4 << 20, "none", 0x20000000 + (2 << 20), 0x20000000, 3, W, W, 0.5, 0.125)
+        want = m.view(0x20000000 + (2 << 20) + 4 * W, np.uint32, W)[1:W - 1]
+        dst = out + 4 * r * W
+        inside = dst + 4 * W <= p.end
+        if not inside:
+            dst = p.base + (dst - p.base) % p.size          # mask = modulo on a pow2 partition
+        got = download(dst, 4 * W).view(np.uint32)[1:W - 1]
+        if inside or mode in ("mask", "modulo", "maskcount"):
+            np.testing.assert_array_equal(got, want, err_msg=f"row {r}")
+        else:
+            assert not got.any(), f"row {r}: a refused store landed"     # scrubbed, never written
+
+
 def test_c4_stencil_v2_full_sampled_rows(arenas):
     """K5 v2 at the BASELINE size in the bench's launch configuration: sampled
     rows (incl. tile edges at 16-row and 248-column boundaries) against the
