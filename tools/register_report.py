@@ -34,7 +34,7 @@ def main():
     table = {}
     for mangled, r in rows.items():
         name = dm[mangled]
-        km = re.search(r"(k_[A-Za-z0-9]+)<(\d)", name)
+        km = re.search(r"(k_[A-Za-z0-9_]+)<(\d)", name)
         if not km:
             continue
         kernel, mode = km.group(1), MODES.get(km.group(2), km.group(2))
