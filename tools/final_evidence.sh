@@ -1,4 +1,7 @@
-cd $GRAFT_REPO_ROOT
+#!/bin/bash
+# Final evidence of a round in one GPU call: every GPU test, smoke, bench.py x 3, the ncu launch
+# list of the bench, ncu --set full of the stencil (hoisted and per access).  Output in gpurun_out/.
+cd "$(dirname "$0")/.."
 NCU=1 bash tools/gpu_round.sh > gpurun_out/fin_round.txt 2>&1
 for i in 2 3; do timeout 900 python bench.py > gpurun_out/bench_$i.json 2> gpurun_out/bench_$i.err; done
 bash tools/ncu_full.sh "stencil:mask stencil:check" > gpurun_out/fin_ncu_h.txt 2>&1
