@@ -183,6 +183,24 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     bool live[S];
     int32_t j[S];
     uint64_t ov[S], tv[S];
+    // Per-access modulo on the streams (SMODE == kModulo: hoisting off): this
+    // thread's index and output addresses increase with k (and g), so when
+    // neither range straddles the base nor spans the partition, each access's
+    // fence follows from the previous one's (Fence::step_up, exactly the full
+    // modulo); otherwise every access takes the full modulo.
+    bool walk = false;
+    if constexpr (SMODE == kModulo) {
+        const uint64_t sl0 = s0, sl1 = s0 + (uint64_t)(S - 1) * kThreads;
+        const uint64_t i0 = row_of<P2>(sl0, tpr, dv), i1 = row_of<P2>(sl1, tpr, dv);
+        const uint64_t lo_i = idx + 4 * i0, hi_i = idx + 4 * i1 + 4;
+        const uint64_t lo_o = out + 16 * (i0 * vpr + (sl0 - i0 * tpr));
+        const uint64_t hi_o = out + 16 * (i1 * vpr + (sl1 - i1 * tpr)) + 16 * tpr * (G - 1) + 16;
+        const auto side = [&](uint64_t lo, uint64_t hi) {
+            return lo <= hi && hi - lo < fd.size && (hi <= fd.base || lo >= fd.base);
+        };
+        walk = side(lo_i, hi_i) && side(lo_o, hi_o);
+    }
+    uint64_t fa_prev = 0, aa_prev = 0;
 #pragma unroll
     for (int k = 0; k < S; k++) {                       // 1. index loads (predicated, no branch:
         const uint64_t sl = s0 + (uint64_t)k * kThreads; //    a branch would serialise them)
@@ -193,7 +211,15 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
         uint32_t ci = 0;
         const bool oki = fi.go_aligned(ai, ci, 1) && live[k];        // ALU only: no branch
         j[k] = 0;
-        if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fi.addr(ai)));
+        uint64_t fa;
+        if constexpr (SMODE == kModulo) {
+            fa = (k == 0 || !walk) ? fi.addr(ai) : fi.step_up(fa_prev, ai - aa_prev);
+            fa_prev = fa;
+            aa_prev = ai;
+        } else {
+            fa = fi.addr(ai);
+        }
+        if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fa));
         if (live[k] && t == 0) nv += ci;                             // one index access per row
         ov[k] = out + 16 * (i * vpr + t);
         tv[k] = 16 * t;
@@ -260,12 +286,24 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
             }
         }
     }
+    uint64_t fo_prev = 0, ao_prev = 0;
 #pragma unroll
     for (int k = 0; k < S; k++) {                       // 4. output stores
         if (live[k]) {
+            if constexpr (SMODE == kModulo) {
+                // live[] is a prefix, so k == 0 is the first store of the walk
+                const uint64_t f0 = (k == 0 || !walk) ? fo.addr(ov[k]) : fo.step_up(fo_prev, ov[k] - ao_prev);
+                fo_prev = f0;
+                ao_prev = ov[k];
 #pragma unroll
-            for (int g = 0; g < G; g++) {
-                vst4(fo, ov[k] + 16 * tpr * g, r[k][g], nv, st_out, st_w);
+                for (int g = 0; g < G; g++)
+                    st_out(g == 0 ? f0 : (walk ? fo.step_up(f0, 16 * tpr * g) : fo.addr(ov[k] + 16 * tpr * g)),
+                           r[k][g]);
+            } else {
+#pragma unroll
+                for (int g = 0; g < G; g++) {
+                    vst4(fo, ov[k] + 16 * tpr * g, r[k][g], nv, st_out, st_w);
+                }
             }
         }
     }

@@ -123,6 +123,36 @@ def test_modulo_stencil_out_crossing_end(arenas, mode):
          None if mode == "modulo" else 6 * (W - 2))
 
 
+@pytest.mark.parametrize("mode", ["modulo", "check"])
+@pytest.mark.parametrize("D", [12, 32, 64])          # row slots: tpr 3 (reciprocal), 8 (shift); G = 1, 1, 2
+@pytest.mark.parametrize("case", ["out_crossing_end", "idx_below_base"])
+def test_modulo_gather_rows_stream_walk(arenas, mode, D, case):
+    """Per access (run again by test_gpu_peraccess.py), the row gather fences
+    its index and output streams by a walk (Fence::step_up) when a thread's
+    ranges neither straddle the base nor span the partition, else by the full
+    modulo.  Both paths against the oracle's u64 remainder: `out` running past
+    the end of a non-power-of-two partition, and `idx` starting below the base
+    (its wrapped half holds valid indices, so every read is race-free)."""
+    a, parts, rng = _setup(arenas, 606)
+    p = parts[1]
+    n = 2048
+    tab = p.base + 1 * MiB
+    j = rng.integers(0, n, n, dtype=np.int64).astype(np.int32)
+    if case == "out_crossing_end":
+        idx, out = p.base + 3 * MiB, p.end - n * 4 * D // 2
+        upload(idx, j)
+    else:
+        idx, out = p.base - 4 * (n // 2), p.base + 6 * MiB
+        upload(p.base, j[n // 2:])
+        # the first half lies below the base: element e is read (modulo) at
+        # base + ((idx + 4e - base) mod 2^64) mod size
+        for e in range(n // 2):
+            upload(p.base + ((idx + 4 * e - p.base) % (1 << 64)) % p.size, j[e:e + 1])
+    _run(a, parts, 1, mode,
+         lambda p: a.gather(p.id, mode, out, tab, idx, n, D),
+         lambda m, p: oracle.gather(m, p.base, p.size, mode, out, tab, idx, n, D))
+
+
 @pytest.mark.parametrize("mode", ["modulo", "check", "clamp"])
 @pytest.mark.parametrize("case", ["in_crossing_end", "in_below_base", "pitch_past_size"])
 def test_modulo_stencil_walk(arenas, mode, case):
