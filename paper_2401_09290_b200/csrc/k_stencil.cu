@@ -188,21 +188,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__
     const uint64_t c = 4ull * ((uint64_t)blockIdx.x * kThreads + threadIdx.x);
     const uint32_t r0 = 1u + blockIdx.y * (uint32_t)ROWS;
     const uint32_t r1 = (r0 + ROWS < H - 1) ? r0 + ROWS : H - 1;
-    if (c < W && r0 < r1) {
-        if constexpr (hoistable(MODE)) {
-            // conservative extents of everything this strip touches; inside the
-            // partition the fence is the identity and nothing is counted
-            const uint64_t lo_in = in + 4 * ((r0 - 1) * pitch + c) - (c ? 4 : 0);
-            const uint64_t hi_in = in + 4 * (r1 * pitch + c + 5);
-            const uint64_t lo_out = out + 4 * (r0 * pitch + c), hi_out = out + 4 * ((r1 - 1) * pitch + c + 4);
-            if (lo_in < hi_in && lo_out < hi_out && range_in(fd, lo_in, hi_in - lo_in) &&
-                range_in(fd, lo_out, hi_out - lo_out))
-                strip<kNone, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
-            else
-                strip<MODE, 1>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
-        } else {
-            strip<MODE, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+    if constexpr (hoistable(MODE)) {
+        // conservative extents of everything the CTA's strip touches (from
+        // blockIdx only, so the test runs on the uniform datapath); inside the
+        // partition the fence is the identity and nothing is counted, so the
+        // whole CTA runs the unfenced body and skips the violation flush
+        const uint64_t cb = 4ull * blockIdx.x * kThreads, ce = cb + 4ull * kThreads;
+        const uint64_t lo_in = in + 4 * ((r0 - 1) * pitch + cb) - (cb ? 4 : 0);
+        const uint64_t hi_in = in + 4 * (r1 * pitch + ce + 1);
+        const uint64_t lo_out = out + 4 * (r0 * pitch + cb), hi_out = out + 4 * ((r1 - 1) * pitch + ce);
+        if (lo_in < hi_in && lo_out < hi_out && range_in(fd, lo_in, hi_in - lo_in) &&
+            range_in(fd, lo_out, hi_out - lo_out)) {
+            if (c < W && r0 < r1) strip<kNone, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+            return;
         }
+        if (c < W && r0 < r1) strip<MODE, 1>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+    } else {
+        if (c < W && r0 < r1) strip<MODE, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
     }
     if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }

@@ -62,9 +62,10 @@ __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ Fence
     const uint64_t v0 = c0 + threadIdx.x;
     if constexpr (hoistable(MODE)) {     // the fence is the identity inside the partition
         const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
-        if (cn && range_in(fd, src + 16 * c0, 16 * cn) && range_in(fd, dst + 16 * c0, 16 * cn))
+        if (cn && range_in(fd, src + 16 * c0, 16 * cn) && range_in(fd, dst + 16 * c0, 16 * cn)) {
             copy_chunk<kNone>(fd, dst, src, v0, nvec, nv);
-        else
+            if (blockIdx.x != 0) return;     // nothing counted: the whole CTA skips the flush
+        } else
             copy_chunk<MODE>(fd, dst, src, v0, nvec, nv);
     } else {
         copy_chunk<MODE>(fd, dst, src, v0, nvec, nv);
@@ -121,9 +122,10 @@ __global__ void __launch_bounds__(kThreads) k_saxpy(const __grid_constant__ Fenc
     const uint64_t v0 = c0 + threadIdx.x;
     if constexpr (hoistable(MODE)) {     // the fence is the identity inside the partition
         const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
-        if (cn && range_in(fd, x + 16 * c0, 16 * cn) && range_in(fd, y + 16 * c0, 16 * cn))
+        if (cn && range_in(fd, x + 16 * c0, 16 * cn) && range_in(fd, y + 16 * c0, 16 * cn)) {
             saxpy_chunk<kNone>(fd, alpha, x, y, v0, nvec, nv);
-        else
+            if (blockIdx.x != 0) return;     // nothing counted: the whole CTA skips the flush
+        } else
             saxpy_chunk<MODE>(fd, alpha, x, y, v0, nvec, nv);
     } else {
         saxpy_chunk<MODE>(fd, alpha, x, y, v0, nvec, nv);
