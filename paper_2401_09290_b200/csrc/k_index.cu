@@ -200,29 +200,42 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
         };
         walk = side(lo_i, hi_i) && side(lo_o, hi_o);
     }
-    uint64_t fa_prev = 0, aa_prev = 0;
+    if constexpr (SMODE == kModulo) {
+        uint64_t fa_prev = 0, aa_prev = 0;
 #pragma unroll
-    for (int k = 0; k < S; k++) {                       // 1. index loads (predicated, no branch:
-        const uint64_t sl = s0 + (uint64_t)k * kThreads; //    a branch would serialise them)
-        live[k] = sl < nslots;
-        const uint64_t i = row_of<P2>(sl, tpr, dv);
-        const uint64_t t = sl - i * tpr;
-        const uint64_t ai = idx + 4 * i;
-        uint32_t ci = 0;
-        const bool oki = fi.go_aligned(ai, ci, 1) && live[k];        // ALU only: no branch
-        j[k] = 0;
-        uint64_t fa;
-        if constexpr (SMODE == kModulo) {
-            fa = (k == 0 || !walk) ? fi.addr(ai) : fi.step_up(fa_prev, ai - aa_prev);
+        for (int k = 0; k < S; k++) {                       // 1. index loads (predicated, no branch:
+            const uint64_t sl = s0 + (uint64_t)k * kThreads; //    a branch would serialise them)
+            live[k] = sl < nslots;
+            const uint64_t i = row_of<P2>(sl, tpr, dv);
+            const uint64_t t = sl - i * tpr;
+            const uint64_t ai = idx + 4 * i;
+            uint32_t ci = 0;
+            const bool oki = fi.go_aligned(ai, ci, 1) && live[k];        // ALU only: no branch
+            j[k] = 0;
+            const uint64_t fa = (k == 0 || !walk) ? fi.addr(ai) : fi.step_up(fa_prev, ai - aa_prev);
             fa_prev = fa;
             aa_prev = ai;
-        } else {
-            fa = fi.addr(ai);
+            if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fa));
+            if (live[k] && t == 0) nv += ci;                             // one index access per row
+            ov[k] = out + 16 * (i * vpr + t);
+            tv[k] = 16 * t;
         }
-        if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fa));
-        if (live[k] && t == 0) nv += ci;                             // one index access per row
-        ov[k] = out + 16 * (i * vpr + t);
-        tv[k] = 16 * t;
+    } else {
+#pragma unroll
+        for (int k = 0; k < S; k++) {                       // 1. index loads (predicated, no branch:
+            const uint64_t sl = s0 + (uint64_t)k * kThreads; //    a branch would serialise them)
+            live[k] = sl < nslots;
+            const uint64_t i = row_of<P2>(sl, tpr, dv);
+            const uint64_t t = sl - i * tpr;
+            const uint64_t ai = idx + 4 * i;
+            uint32_t ci = 0;
+            const bool oki = fi.go_aligned(ai, ci, 1) && live[k];        // ALU only: no branch
+            j[k] = 0;
+            if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fi.addr(ai)));
+            if (live[k] && t == 0) nv += ci;                             // one index access per row
+            ov[k] = out + 16 * (i * vpr + t);
+            tv[k] = 16 * t;
+        }
     }
     // (clamp: a warp-synchronising point after the index loads keeps ptxas
     // from consuming each loaded index before the next load issues)
