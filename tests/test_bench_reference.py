@@ -22,3 +22,17 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in d["config"]
+
+
+def test_json_line_survives_stdout_noise():
+    """The GPU arm routes fd 1 to stderr (NCCL prints its version line to
+    stdout at communicator setup) and writes its one JSON line to the saved
+    stdout: Python prints, C-level writes and child processes all land on
+    stderr, the JSON line alone on stdout."""
+    code = ("import os, bench; bench.quiet_stdout(); print('python noise'); os.write(1, b'fd noise\\n'); "
+            "os.system('echo child noise'); bench.emit({'metric': 'm', 'value': 1.0}); print('late noise')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.splitlines() == ['{"metric": "m", "value": 1.0}']
+    for noise in ("python noise", "fd noise", "child noise", "late noise"):
+        assert noise in r.stderr
