@@ -29,6 +29,10 @@
  *  - Thread safety: arena mutations (partition alloc/free, malloc/free) are
  *    serialised by an internal mutex; launches read an immutable snapshot of
  *    the partition bounds entry and may be issued from several threads.
+ *    Partition alloc/free wait until no launch, checked transfer, fill or
+ *    graph replay is between its bounds snapshot and its enqueue, and free
+ *    synchronises the device before it unmaps: work is never enqueued with
+ *    bounds of a partition that no longer exists.
  */
 #ifndef GUARDIAN_H
 #define GUARDIAN_H
@@ -90,6 +94,18 @@ typedef enum {
     GD_MODE_NONE = 0, GD_MODE_MASK = 1, GD_MODE_CHECK = 2, GD_MODE_MODULO = 3,
     GD_MODE_MASK_COUNT = 4, GD_MODE_CLAMP = 5
 } gd_mode;
+
+/* Per-access flag, OR-ed into the mode of any launch (gd_launch_fenced_*,
+ * gd_work.mode): fence every access one by one, as the paper's instrumented
+ * kernels do ("before every load and store"; §4.3), instead of
+ * the default tile-level range test that runs the unfenced body on tiles
+ * wholly inside the partition (reading R-hoist).  Results and
+ * violation counts are identical either way; only the cost differs.  The
+ * descriptor-fenced TMA kernels (GEMM, K5 v2) have no per-access fence and
+ * ignore it; MASK is always per access.  Setting GD_CHECK_PER_ACCESS=1 in the
+ * environment forces it for every launch of the process.  Any other bit
+ * above the mode is GD_ERR_INVALID_ARG.                                      */
+#define GD_FENCE_PER_ACCESS 0x100u
 
 /* Kernel kinds (index of the per-kind statistics).                            */
 typedef enum {
@@ -310,7 +326,9 @@ typedef struct gd_graph gd_graph;     /* opaque, library-owned */
 gd_status gd_graph_create(gd_arena *a, const gd_work *items, uint32_t n_items, uint32_t n_streams, gd_graph **out);
 /* Replay the captured step on `stream` with one host call.  Refuses with
  * UNKNOWN_PARTITION (nothing launched) if any partition the graph fences was
- * freed or re-allocated since capture: stale bounds are never used.        */
+ * freed or re-allocated since capture: stale bounds are never used; and, for
+ * a graph that captured unfenced solo launches (gd_arena_set_native_when_solo),
+ * if the arena's partition set or that switch changed since capture.        */
 gd_status gd_graph_launch(gd_graph *g, void *stream);
 gd_status gd_graph_destroy(gd_graph *g);
 
@@ -330,12 +348,17 @@ int gd_last_cuda_error(void);
  * default off).  While on and exactly one partition of the arena is live,
  * every launch is validated in its requested mode and then run as
  * GD_MODE_NONE: no fence and nothing counted.  A second live partition
- * restores fencing for the next launch.                                      */
+ * restores fencing for the next launch: the decision is taken and the kernel
+ * enqueued while partition changes are held off, and a new partition is
+ * scrubbed only after every enqueued kernel has finished.  A graph captured
+ * while a tenant ran alone is refused at replay (UNKNOWN_PARTITION) once any
+ * partition was allocated or freed, or this switch changed, since capture.  */
 gd_status gd_arena_set_native_when_solo(gd_arena *a, int on);
 
 /* Synchronises, then reports (and clears) device-side health flags:
- * bit 0 = a tensor-core pipeline wait timed out (the kernel gave up instead
- * of hanging the shared context).                                            */
+ * bit 0 = a tensor-core (GEMM) pipeline wait timed out, bit 1 = a TMA load
+ * wait of the K5 v2 stencil timed out (the kernel gave up after ~2 s instead
+ * of hanging the shared context; the tile was not stored).                   */
 gd_status gd_device_flags(gd_arena *a, uint32_t *flags);
 /* Library build identification, e.g. "guardian sm_100a <git>".               */
 const char *gd_version(void);

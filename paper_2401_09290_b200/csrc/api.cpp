@@ -10,6 +10,7 @@
 
 #include <cstring>
 #include <mutex>
+#include <shared_mutex>
 
 #include "arena.h"
 #include "drv.h"
@@ -258,6 +259,7 @@ extern "C" gd_status gd_arena_destroy(gd_arena *a) {
         if (a->vmm) drv().MemAddressFree((CUdeviceptr)a->reserve_va, a->reserve_size);
         if (a->d_stats) cudaFree(a->d_stats);
         if (a->zero_buf) cudaFree(a->zero_buf);
+        for (void *z : a->zero_retired) cudaFree(z);
     }
     delete a;
     return GD_OK;
@@ -313,9 +315,13 @@ gd_status carve(gd_arena *a, uint64_t size, bool pow2, gd_partition_info *out) {
             give_back();
             return st;
         }
-        // scrub (reading A15) and zero this tenant's counters
+        // scrub (reading A15) and zero this tenant's counters.  Everything
+        // already enqueued finishes first: a kernel of a tenant that ran alone
+        // unfenced (native when solo) must not write the new partition after
+        // its scrub.
         Geom g{a->sms};
-        cudaError_t e = launch_fill(b, 0, size, 0, 0, g);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e == cudaSuccess) e = launch_fill(b, 0, size, 0, 0, g);
         if (e == cudaSuccess)
             e = cudaMemset(a->d_stats + (uint64_t)id * GD_NUM_KINDS, 0, sizeof(unsigned long long) * GD_NUM_KINDS);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -332,6 +338,7 @@ gd_status carve(gd_arena *a, uint64_t size, bool pow2, gd_partition_info *out) {
     p.order = order;
     p.pow2 = pow2;
     p.gen = a->next_gen++;
+    a->epoch++;
     p.sub.init(size);
     for (unsigned k = 0; k < GD_NUM_KINDS; k++) a->host[id][k] = HostCounters{};
     fill_info(id, p, out);
@@ -344,6 +351,7 @@ extern "C" gd_status gd_partition_alloc(gd_arena *a, uint64_t requested, gd_part
     if (!a || !out || requested == 0 || requested > a->size) return GD_ERR_INVALID_ARG;
     uint64_t size = GD_MIN_PARTITION;
     while (size < requested) size <<= 1;                 // next pow2 >= max(req, 4 KiB)
+    std::unique_lock<std::shared_mutex> guard(a->launch_mu);
     std::lock_guard<std::mutex> lk(a->mu);
     return carve(a, size, true, out);
 }
@@ -353,12 +361,15 @@ extern "C" gd_status gd_partition_alloc_exact(gd_arena *a, uint64_t requested, g
     const uint64_t g = a->vmm ? a->gran : GD_MIN_PARTITION;     // physical backing granule
     uint64_t size = (requested + g - 1) / g * g;
     if (size < GD_MIN_PARTITION) size = GD_MIN_PARTITION;
+    std::unique_lock<std::shared_mutex> guard(a->launch_mu);
     std::lock_guard<std::mutex> lk(a->mu);
     return carve(a, size, (size & (size - 1)) == 0, out);
 }
 
 extern "C" gd_status gd_partition_free(gd_arena *a, uint32_t id) {
     if (!a) return GD_ERR_INVALID_ARG;
+    // exclusive: no launch sits between its bounds snapshot and its enqueue
+    std::unique_lock<std::shared_mutex> guard(a->launch_mu);
     std::lock_guard<std::mutex> lk(a->mu);
     if (id >= GD_MAX_TENANTS || !a->parts[id].live) return GD_ERR_UNKNOWN_PARTITION;
     Partition &p = a->parts[id];
@@ -370,6 +381,7 @@ extern "C" gd_status gd_partition_free(gd_arena *a, uint32_t id) {
     if (p.pow2) a->buddy.free(p.base - a->base, p.order);
     else a->buddy.free_exact(p.base - a->base, p.size);
     p.live = false;
+    a->epoch++;
     return GD_OK;
 }
 
@@ -427,6 +439,7 @@ extern "C" gd_status gd_memcpy_h2d(gd_arena *a, uint32_t id, uint64_t dst, const
                                    void *stream) {
     if (!a || (!src && n)) return GD_ERR_INVALID_ARG;
     if (a->device < 0) return GD_ERR_UNSUPPORTED;
+    std::shared_lock<std::shared_mutex> guard(a->launch_mu);    // bounds stay valid until enqueued
     uint64_t b, s;
     gd_status st = snapshot(a, id, &b, &s);
     if (st != GD_OK) return st;
@@ -440,6 +453,7 @@ extern "C" gd_status gd_memcpy_h2d(gd_arena *a, uint32_t id, uint64_t dst, const
 extern "C" gd_status gd_memcpy_d2h(gd_arena *a, uint32_t id, void *dst, uint64_t src, uint64_t n, void *stream) {
     if (!a || (!dst && n)) return GD_ERR_INVALID_ARG;
     if (a->device < 0) return GD_ERR_UNSUPPORTED;
+    std::shared_lock<std::shared_mutex> guard(a->launch_mu);    // bounds stay valid until enqueued
     uint64_t b, s;
     gd_status st = snapshot(a, id, &b, &s);
     if (st != GD_OK) return st;
@@ -453,6 +467,7 @@ extern "C" gd_status gd_memcpy_d2h(gd_arena *a, uint32_t id, void *dst, uint64_t
 extern "C" gd_status gd_memcpy_d2d(gd_arena *a, uint32_t id, uint64_t dst, uint64_t src, uint64_t n, void *stream) {
     if (!a) return GD_ERR_INVALID_ARG;
     if (a->device < 0) return GD_ERR_UNSUPPORTED;
+    std::shared_lock<std::shared_mutex> guard(a->launch_mu);    // bounds stay valid until enqueued
     uint64_t b, s;
     gd_status st = snapshot(a, id, &b, &s);
     if (st != GD_OK) return st;
@@ -467,6 +482,7 @@ extern "C" gd_status gd_partition_fill(gd_arena *a, uint32_t id, uint32_t patter
                                        uint64_t nbytes, void *stream) {
     if (!a || pattern > 1) return GD_ERR_INVALID_ARG;
     if (a->device < 0) return GD_ERR_UNSUPPORTED;
+    std::shared_lock<std::shared_mutex> guard(a->launch_mu);    // bounds stay valid until enqueued
     uint64_t b, s;
     gd_status st = snapshot(a, id, &b, &s);
     if (st != GD_OK) return st;
@@ -488,11 +504,21 @@ namespace gd {
 
 // Validate `w` (dry) or validate and launch it.  Structural errors are
 // returned before anything is issued.
-gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool dry, bool account,
-                   uint64_t *bytes_out, uint64_t *flops_out) {
+gd_status run_work_locked(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool dry, bool account,
+                          LaunchOut *out) {
     if (!a) return GD_ERR_INVALID_ARG;
     gd_work w = w_in;
-    if (w.mode > GD_MODE_CLAMP || w.kind >= GD_NUM_KINDS) return GD_ERR_INVALID_ARG;
+    if ((w.mode & ~(kModeMask | GD_FENCE_PER_ACCESS)) || base_mode(w.mode) > GD_MODE_CLAMP || w.kind >= GD_NUM_KINDS)
+        return GD_ERR_INVALID_ARG;
+    // GD_FENCE_PER_ACCESS: no tile-level range test (the paper's per-access
+    // instrumentation; identical results); GD_CHECK_PER_ACCESS=1 forces it
+    // for every launch of the process
+    static const bool env_pa = [] {
+        const char *e = getenv("GD_CHECK_PER_ACCESS");
+        return e && e[0] == '1';
+    }();
+    const bool per_access = env_pa || (w.mode & GD_FENCE_PER_ACCESS);
+    w.mode = base_mode(w.mode);
     uint64_t base, size;
     gd_status st = snapshot(a, w.tenant, &base, &size);
     if (st != GD_OK) return st;
@@ -557,7 +583,11 @@ gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool d
     // PAPER.md:175 "when an application runs alone ... issues a native kernel"
     // (SPEC.md:418 --native-when-solo, off by default): validated as requested,
     // run unfenced
-    if (w.mode != GD_MODE_NONE && solo_native(a)) w.mode = GD_MODE_NONE;
+    // (the caller's shared hold of launch_mu keeps the partition count fixed
+    // until this launch is enqueued; a later carve synchronises before it
+    // scrubs, so the unfenced kernel cannot reach the new partition)
+    const bool solo = w.mode != GD_MODE_NONE && solo_native(a);
+    if (solo) w.mode = GD_MODE_NONE;
 
     FenceDesc fd;
     fd.base = base;
@@ -565,13 +595,7 @@ gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool d
     fd.size = size;
     fd.inv = recip64(size);
     fd.viol = a->d_stats + (uint64_t)w.tenant * GD_NUM_KINDS + w.kind;
-    // GD_CHECK_PER_ACCESS=1: no tile-level range test (measures the paper's
-    // per-access check cost; results are identical either way)
-    static const uint32_t no_hoist = [] {
-        const char *e = getenv("GD_CHECK_PER_ACCESS");
-        return (e && e[0] == '1') ? kNoHoist : 0u;
-    }();
-    fd.flags = no_hoist;
+    fd.flags = per_access ? kNoHoist : 0u;
     fd.pad_ = 0;
     const Geom g{a->sms};
     DeviceGuard dg(a->device);
@@ -602,8 +626,11 @@ gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool d
         }
     }
     if (e != cudaSuccess) return cuda_fail(e);
-    if (bytes_out) *bytes_out = bytes;
-    if (flops_out) *flops_out = flops;
+    if (out) {
+        out->bytes = bytes;
+        out->flops = flops;
+        out->solo = solo;
+    }
     if (account) {
         std::lock_guard<std::mutex> lk(a->mu);
         HostCounters &hc = a->host[w.tenant][w.kind];
@@ -612,6 +639,12 @@ gd_status run_work(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool d
         hc.flops += flops;
     }
     return GD_OK;
+}
+
+gd_status run_work(gd_arena *a, const gd_work &w, cudaStream_t stream, bool dry) {
+    if (!a) return GD_ERR_INVALID_ARG;
+    std::shared_lock<std::shared_mutex> guard(a->launch_mu);
+    return run_work_locked(a, w, stream, dry);
 }
 
 gd_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GD_OK : cuda_fail(e); }
@@ -804,8 +837,10 @@ extern "C" int gd_last_cuda_error(void) { return g_last_cuda; }
 
 extern "C" gd_status gd_arena_set_native_when_solo(gd_arena *a, int on) {
     if (!a) return GD_ERR_INVALID_ARG;
+    std::unique_lock<std::shared_mutex> guard(a->launch_mu);
     std::lock_guard<std::mutex> lk(a->mu);
     a->native_when_solo = on != 0;
+    a->epoch++;                                       // graphs captured under the old rule go stale
     return GD_OK;
 }
 
@@ -816,7 +851,7 @@ extern "C" gd_status gd_device_flags(gd_arena *a, uint32_t *flags) {
     DeviceGuard dg(a->device);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e);
-    *flags = gemm_timeout_flag() ? 1u : 0u;
+    *flags = (gemm_timeout_flag() ? 1u : 0u) | (stencil_tma_timeout_flag() ? 2u : 0u);
     return GD_OK;
 }
 

@@ -4,6 +4,7 @@
 #include <map>
 #include <mutex>
 #include <set>
+#include <shared_mutex>
 #include <vector>
 
 #include "guardian.h"
@@ -80,8 +81,16 @@ struct gd_arena {
     unsigned long long *d_stats = nullptr;  // u64[GD_MAX_TENANTS][GD_NUM_KINDS], outside the arena
     void *zero_buf = nullptr;        // trusted zero row for operands with no rows (gemm.cu)
     uint64_t zero_bytes = 0;
+    std::vector<void *> zero_retired;  // outgrown zero rows: captured graphs may still read them (freed at destroy)
     int sms = 148;
     uint64_t next_gen = 1;
     bool native_when_solo = false;   // a tenant alone runs the native kernel
-    std::mutex mu;
+    uint64_t epoch = 0;              // bumped by every carve / free / native_when_solo change
+    std::mutex mu;                   // bounds table, allocators, counters
+    // Launch guard: every path that snapshots partition bounds and enqueues
+    // work with them (launches, checked transfers, fills, graph replays)
+    // holds it shared from the snapshot until the work is enqueued; carve and
+    // free hold it exclusively, so bounds never change between a snapshot and
+    // its enqueue (free then synchronises before it unmaps).  Taken before mu.
+    std::shared_mutex launch_mu;
 };

@@ -539,17 +539,24 @@ uint64_t desc_rows(int mode, uint64_t base, uint64_t size, uint64_t p, uint64_t 
 
 // Trusted all-zero row of >= 2K bytes outside every partition (allocating
 // synchronises, so graph capture calls gemm_prepare first).
-gd_status ensure_zero_row(gd_arena *a, uint64_t K) {
+gd_status ensure_zero_row(gd_arena *a, uint64_t K, uint64_t *zp) {
     std::lock_guard<std::mutex> lk(a->mu);
-    if (a->zero_bytes >= 2ull * K) return GD_OK;
-    if (a->zero_buf) cudaFree(a->zero_buf);
-    a->zero_buf = nullptr;
-    a->zero_bytes = 0;
-    cudaError_t e = cudaMalloc(&a->zero_buf, 2ull * K);
-    if (e == cudaSuccess) e = cudaMemset(a->zero_buf, 0, 2ull * K);
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) return cuda_status(e);
-    a->zero_bytes = 2ull * K;
+    if (a->zero_bytes < 2ull * K) {
+        // grow-only: the outgrown row stays allocated (a captured graph's
+        // tensor map may still point at it) until the arena is destroyed
+        void *nb = nullptr;
+        cudaError_t e = cudaMalloc(&nb, 2ull * K);
+        if (e == cudaSuccess) e = cudaMemset(nb, 0, 2ull * K);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            if (nb) cudaFree(nb);
+            return cuda_status(e);
+        }
+        if (a->zero_buf) a->zero_retired.push_back(a->zero_buf);
+        a->zero_buf = nb;
+        a->zero_bytes = 2ull * K;
+    }
+    if (zp) *zp = (uint64_t)a->zero_buf;
     return GD_OK;
 }
 
@@ -594,10 +601,11 @@ gd_status gemm_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uint64_t s
     if (rA == 0 || rB == 0) {
         // an operand with no rows reads as zeros: point its map at a trusted
         // zero row outside every partition
-        gd_status zs = ensure_zero_row(a, K);
+        uint64_t zp = 0;
+        gd_status zs = ensure_zero_row(a, K, &zp);
         if (zs != GD_OK) return zs;
-        if (rA == 0) { Af = (uint64_t)a->zero_buf; rA = 1; ldA = K; }
-        if (rB == 0) { Bf = (uint64_t)a->zero_buf; rB = 1; ldB = K; }
+        if (rA == 0) { Af = zp; rA = 1; ldA = K; }
+        if (rB == 0) { Bf = zp; rB = 1; ldB = K; }
     }
     CUtensorMap tmA, tmB, tmC;
     std::memset(&tmA, 0, sizeof(tmA));

@@ -11,6 +11,8 @@
 // re-allocated -- stale bounds are never used.
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <shared_mutex>
 #include <vector>
 
 #include "dispatch.h"
@@ -29,6 +31,8 @@ struct gd_graph {
         uint64_t bytes, flops;
     };
     std::vector<Cost> costs;                                // host accounting per replay
+    bool solo = false;                                      // captured unfenced solo launches
+    uint64_t epoch = 0;                                     // the arena's epoch at capture
 };
 
 namespace {
@@ -49,8 +53,14 @@ extern "C" gd_status gd_graph_create(gd_arena *a, const gd_work *items, uint32_t
     if (a->device < 0) return GD_ERR_UNSUPPORTED;
     gd_graph *g = new gd_graph();
     g->arena = a;
+    // partitions stay as validated until the capture is complete
+    std::shared_lock<std::shared_mutex> guard(a->launch_mu);
+    {
+        std::lock_guard<std::mutex> lk(a->mu);
+        g->epoch = a->epoch;
+    }
     for (uint32_t i = 0; i < n_items; i++) {              // validate everything first
-        gd_status st = gd::run_work(a, items[i], nullptr, true);
+        gd_status st = gd::run_work_locked(a, items[i], nullptr, true);
         if (st != GD_OK) {
             destroy(g);
             return st;
@@ -61,8 +71,9 @@ extern "C" gd_status gd_graph_create(gd_arena *a, const gd_work *items, uint32_t
         for (auto &u : g->uses) seen = seen || u.id == items[i].tenant;
         if (!seen) g->uses.push_back({items[i].tenant, gen});
         if (items[i].kind == GD_KIND_GEMM || (items[i].kind == GD_KIND_STENCIL && items[i].u32[2] == 1)) {
-            st = items[i].kind == GD_KIND_GEMM ? gd::gemm_prepare(a, items[i], base, size)
-                                               : gd::stencil_tma_prepare(a, items[i], base, size);
+            gd_work w = items[i];
+            w.mode = gd::base_mode(w.mode);
+            st = w.kind == GD_KIND_GEMM ? gd::gemm_prepare(a, w, base, size) : gd::stencil_tma_prepare(a, w, base, size);
             if (st != GD_OK) {
                 destroy(g);
                 return st;
@@ -97,9 +108,10 @@ extern "C" gd_status gd_graph_create(gd_arena *a, const gd_work *items, uint32_t
         for (uint32_t k = 0; k < n_items && st == GD_OK; k++) {
             const gd_work &w = items[order[k]];
             const uint32_t r = rank_of[w.tenant];
-            uint64_t bytes = 0, flops = 0;
-            st = gd::run_work(a, w, streams[r % n_streams], false, false, &bytes, &flops);
-            g->costs.push_back({w.tenant, w.kind, bytes, flops});
+            gd::LaunchOut lo;
+            st = gd::run_work_locked(a, w, streams[r % n_streams], false, false, &lo);
+            g->costs.push_back({w.tenant, w.kind, lo.bytes, lo.flops});
+            g->solo = g->solo || lo.solo;
         }
         // join
         for (uint32_t s = 0; s < n_streams; s++) {
@@ -126,6 +138,12 @@ extern "C" gd_status gd_graph_create(gd_arena *a, const gd_work *items, uint32_t
 
 extern "C" gd_status gd_graph_launch(gd_graph *g, void *stream) {
     if (!g || !g->exec) return GD_ERR_INVALID_ARG;
+    // bounds checked and the replay enqueued with partition changes held off
+    std::shared_lock<std::shared_mutex> guard(g->arena->launch_mu);
+    if (g->solo) {                                        // unfenced solo kernels: only while still alone
+        std::lock_guard<std::mutex> lk(g->arena->mu);
+        if (g->arena->epoch != g->epoch) return GD_ERR_UNKNOWN_PARTITION;
+    }
     for (const auto &u : g->uses) {                       // never replay with stale bounds
         uint64_t base, size, gen;
         if (gd::partition_snapshot(g->arena, u.id, &base, &size, &gen) != GD_OK || gen != u.gen)

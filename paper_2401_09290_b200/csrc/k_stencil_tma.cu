@@ -44,6 +44,39 @@ constexpr uint32_t kSmem = kInBytes + kOutBytes + 16 + 128;     // + 2 mbarriers
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+__device__ unsigned int g_stencil_tma_timeout = 0;   // set if a bounded wait expired
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Wait for phase 0 of `bar`; give up after ~2 s and raise the device flag
+// (gd_device_flags bit 1) instead of hanging every tenant of the shared
+// context on a TMA load that never completes.
+__device__ __forceinline__ bool mbar_wait0(uint32_t bar) {
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0;; spin++) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar)
+            : "memory");
+        if (done) return true;
+        if ((spin & 1023u) == 0) {
+            const uint64_t now = globaltimer();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 2000000000ull) break;
+        }
+    }
+    atomicExch(&g_stencil_tma_timeout, 1u);
+    return false;
+}
+
 __global__ void __launch_bounds__(kThreads) k_stencil_tma(const __grid_constant__ CUtensorMap tmIn,
                                                           const __grid_constant__ CUtensorMap tmOut, float c0,
                                                           float c1, uint32_t gx, uint32_t w1, uint32_t W,
@@ -76,18 +109,14 @@ __global__ void __launch_bounds__(kThreads) k_stencil_tma(const __grid_constant_
         }
     }
     __syncthreads();                                                   // barriers initialised before anyone waits
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tW0: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W0;\n\t}" ::"r"(
-            smem_u32(&bar[0]))
-        : "memory");
-    if (bx == 0 && w1 > 0)
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tW1: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W1;\n\t}" ::"r"(
-                smem_u32(&bar[1]))
-            : "memory");
+    bool ready = mbar_wait0(smem_u32(&bar[0]));
+    if (bx == 0 && w1 > 0) ready = mbar_wait0(smem_u32(&bar[1])) && ready;
+    // a timed-out tile computes and stores nothing (its shared memory is not
+    // the data); the CTA-uniform decision keeps the barrier below reachable
+    ready = __syncthreads_and(ready);
     const int c = threadIdx.x;                                         // out column X + c
     const uint32_t x = (uint32_t)X + (uint32_t)c;
-    if (c < kBW && x != 0) {
+    if (ready && c < kBW && x != 0) {
         // halo box column c + 4 is out column X + c
         float n = tin[c + 4], cc = tin[kInW + c + 4];
 #pragma unroll 4
@@ -109,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) k_stencil_tma(const __grid_constant_
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");      // generic writes -> TMA reads
     __syncthreads();
-    if (threadIdx.x == 0 && (uint32_t)X < w1) {
+    if (ready && threadIdx.x == 0 && (uint32_t)X < w1) {
         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmOut),
                      "r"(smem_u32(tout)), "r"(X), "r"(y0)
                      : "memory");
@@ -134,6 +163,14 @@ bool map_f32(CUtensorMap *m, uint64_t addr, uint64_t cols, uint64_t rows, uint64
 }
 
 }  // namespace
+
+// Read-and-clear the device timeout flag of k_stencil_tma.
+unsigned int stencil_tma_timeout_flag() {
+    unsigned int v = 0, z = 0;
+    cudaMemcpyFromSymbol(&v, g_stencil_tma_timeout, sizeof(v));
+    cudaMemcpyToSymbol(g_stencil_tma_timeout, &z, sizeof(z));
+    return v;
+}
 
 // Everything stencil_tma_dispatch might do outside a stream (graph capture).
 gd_status stencil_tma_prepare(gd_arena *a, const gd_work &w, uint64_t base, uint64_t size) {
@@ -169,7 +206,8 @@ gd_status stencil_tma_dispatch(gd_arena *a, const gd_work &w, uint64_t base, uin
     if (st != GD_OK) return st;
     uint64_t in_pitch = pitch;
     if (rin == 0) {                                     // no readable row: every input reads as zero
-        inf = (uint64_t)a->zero_buf;
+        st = ensure_zero_row(a, 2 * W, &inf);
+        if (st != GD_OK) return st;
         rin = 1;
         in_pitch = (W + 3) & ~3ull;
     }

@@ -34,5 +34,6 @@ cudaError_t launch_fill(uint64_t base, uint64_t offset, uint64_t nbytes, uint32_
 uint64_t desc_rows(int mode, uint64_t base, uint64_t size, uint64_t p, uint64_t rows, uint64_t rowbytes,
                    uint64_t stride, uint64_t *pf);
 unsigned int gemm_timeout_flag();
+unsigned int stencil_tma_timeout_flag();
 
 }  // namespace gd

@@ -6,6 +6,8 @@
 // kernels (spatial sharing).
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <shared_mutex>
 #include <vector>
 
 #include "dispatch.h"
@@ -97,8 +99,13 @@ extern "C" gd_status gd_launcher_run_policy(gd_arena *a, const gd_work *items, u
     if (!a || ((!items) && n_items)) return GD_ERR_INVALID_ARG;
     if (n_items && (!streams || n_streams == 0)) return GD_ERR_INVALID_ARG;
     if (policy > GD_POLICY_MEMORY_LANE) return GD_ERR_INVALID_ARG;
+    // Held shared from validation to the last enqueue: no partition can be
+    // allocated or freed in between, so every item is issued with the bounds
+    // it was validated against and a validated step is issued whole (only a
+    // CUDA error can stop it part-way).
+    std::shared_lock<std::shared_mutex> hold(a->launch_mu);
     for (uint32_t i = 0; i < n_items; i++) {          // nothing is issued unless everything is valid
-        gd_status st = gd::run_work(a, items[i], nullptr, true);
+        gd_status st = gd::run_work_locked(a, items[i], nullptr, true);
         if (st != GD_OK) return st;
     }
     std::vector<uint32_t> order(n_items), tenants, rank;
@@ -129,7 +136,7 @@ extern "C" gd_status gd_launcher_run_policy(gd_arena *a, const gd_work *items, u
         if (e == cudaSuccess && lane_on && c != kTensorCls && lane_live)
             e = cudaStreamWaitEvent(s, lane, 0);
         if (e != cudaSuccess) return gd::cuda_status(e);
-        gd_status st = gd::run_work(a, items[i], s, false);
+        gd_status st = gd::run_work_locked(a, items[i], s, false);
         if (st != GD_OK) return st;
         if (sep && c != kStreamCls) e = ce.record(c, si, s);
         if (e == cudaSuccess && lane_on && c != kTensorCls) {

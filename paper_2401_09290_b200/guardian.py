@@ -24,6 +24,7 @@ STATUS = ["GD_OK", "GD_ERR_INVALID_ARG", "GD_ERR_NOT_POW2", "GD_ERR_DEVICE_OOM",
  GD_ERR_UNKNOWN_ALLOC, GD_ERR_ALIGN, GD_ERR_OOB_RANGE, GD_ERR_UNSUPPORTED, GD_ERR_CUDA) = range(1, 11)
 GD_MODE_NONE, GD_MODE_MASK, GD_MODE_CHECK = 0, 1, 2
 GD_MODE_MODULO, GD_MODE_MASK_COUNT, GD_MODE_CLAMP = 3, 4, 5
+GD_FENCE_PER_ACCESS = 0x100       # OR-ed into a mode: fence every access (no tile-level range test)
 MODES = {"none": GD_MODE_NONE, "mask": GD_MODE_MASK, "check": GD_MODE_CHECK, "modulo": GD_MODE_MODULO,
          "maskcount": GD_MODE_MASK_COUNT, "clamp": GD_MODE_CLAMP}
 GD_POLICY_ROUND_ROBIN, GD_POLICY_NO_TENSOR_RANDOM, GD_POLICY_MEMORY_LANE = 0, 1, 2
@@ -151,7 +152,14 @@ def _stream(s) -> int | None:
 
 
 def _mode(m) -> int:
-    return MODES[m] if isinstance(m, str) else int(m)
+    """A mode name ("check"), optionally with the per-access suffix
+    ("check+pa" = GD_MODE_CHECK | GD_FENCE_PER_ACCESS), or an int."""
+    if isinstance(m, str):
+        name, _, flag = m.partition("+")
+        if flag not in ("", "pa"):
+            raise ValueError(f"unknown mode suffix in {m!r}")
+        return MODES[name] | (GD_FENCE_PER_ACCESS if flag else 0)
+    return int(m)
 
 
 # --- the C names, one-to-one (status codes returned) -------------------------

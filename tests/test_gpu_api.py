@@ -186,3 +186,41 @@ def test_native_when_solo():
         a.gather(p.id, "check", p.base + 2 * MiB, p.base, p.base + MiB, 2)
         assert a.stats(p.id)["violations"] == 1                      # off: fenced even when alone
     del buf
+
+
+def test_launches_and_partition_changes_from_two_threads(arenas):
+    """partition alloc / free never run between a launch's
+    bounds snapshot and its enqueue.  One thread issues fenced copies into its
+    partition while another allocates and frees a neighbour as fast as it
+    can; no launch may fault (a stale base would hit unmapped memory) and the
+    copies stay correct."""
+    import threading
+    a = arenas(64 * MiB)
+    p = a.partition_alloc(8 * MiB)
+    src = np.arange(MiB // 4, dtype=np.uint32)
+    upload(p.base, src)
+    s = torch.cuda.Stream()
+    stop = threading.Event()
+    errors = []
+
+    def churn():
+        try:
+            while not stop.is_set():
+                q = a.partition_alloc(8 * MiB)
+                a.partition_free(q.id)
+        except Exception as e:          # noqa: BLE001
+            errors.append(e)
+
+    t = threading.Thread(target=churn)
+    t.start()
+    try:
+        for k in range(2000):
+            a.copy(p.id, "check", p.base + MiB * (1 + k % 6), p.base, MiB, stream=s)
+    finally:
+        stop.set()
+        t.join()
+    s.synchronize()
+    assert not errors, errors
+    assert a.stats(p.id)["violations"] == 0
+    for k in range(1, 7):
+        assert np.array_equal(download(p.base + k * MiB, MiB).view(np.uint32), src)

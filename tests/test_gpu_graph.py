@@ -94,3 +94,64 @@ def test_graph_is_cheaper_for_small_steps(arenas):
     print(f"64-kernel step: launcher {t_launcher * 1e6:.1f} us, graph {t_graph * 1e6:.1f} us")
     assert t_graph < t_launcher
     graph.close()
+
+
+def test_graph_captured_solo_goes_stale():
+    """a graph captured while a tenant ran alone with
+    native-when-solo holds unfenced kernels, so it may replay only while the
+    arena's partition set and the switch are unchanged; a graph of fenced
+    kernels keeps replaying while its own partitions stand."""
+    MiB = 1 << 20
+    S = 16 * MiB
+    buf = torch.empty(2 * S, dtype=torch.uint8, device="cuda")
+    base = (buf.data_ptr() + S - 1) & ~(S - 1)
+    with g.Arena.wrap(0, base, S) as a:
+        a.set_native_when_solo(True)
+        p = a.partition_alloc(S // 4)
+        beyond = S // 2
+        upload(base + beyond, np.arange(1024, dtype=np.uint32))
+        upload(p.base + MiB, np.array([(beyond // 4) + 7, 3], dtype=np.int32))
+        item = g.work(p.id, g.GD_KIND_GATHER, "check", ptr=(p.base + 2 * MiB, p.base, p.base + MiB), u64=(2,),
+                      u32=(1,))
+        solo = a.graph([item], n_streams=1)
+        solo.launch()
+        assert download(p.base + 2 * MiB, 8).view(np.uint32)[0] == 7      # native: read through
+        q = a.partition_alloc(S // 4)                                      # a second tenant arrives
+        with pytest.raises(g.GuardianError) as e:
+            solo.launch()
+        assert e.value.status == g.GD_ERR_UNKNOWN_PARTITION
+        fenced = a.graph([item], n_streams=1)                              # captured fenced (two live)
+        a.partition_free(q.id)
+        with pytest.raises(g.GuardianError):                               # alone again: still stale
+            solo.launch()
+        upload(p.base + 2 * MiB, np.zeros(2, np.uint32))
+        fenced.launch()                                                    # fenced graph: still valid
+        assert download(p.base + 2 * MiB, 8).view(np.uint32)[0] == 0
+        solo2 = a.graph([item], n_streams=1)
+        a.set_native_when_solo(False)                                      # the switch changes: stale
+        with pytest.raises(g.GuardianError):
+            solo2.launch()
+        for gr in (solo, fenced, solo2):
+            gr.close()
+    del buf
+
+
+def test_zero_row_growth_keeps_captured_graphs_valid(arenas):
+    """a GEMM whose A has no legal row reads a trusted zero
+    row; a later launch that needs a longer row grows it without freeing the
+    old one, so a graph captured earlier still reads zeros."""
+    a = arenas(64 << 20)
+    p = a.partition_alloc(64 << 20)
+    M = N = 128
+    C, B = p.base, p.base + (1 << 20)
+    upload(B, (np.ones((N, 256), np.float32).view(np.uint32) >> 16).astype(np.uint16))
+    bad_A = p.base - (4 << 20)                                             # below the base: no legal row
+    small = g.work(p.id, g.GD_KIND_GEMM, "check", ptr=(C, bad_A, B), u64=(64, 256, N), u32=(M, N, 64))
+    gr = a.graph([small], n_streams=1)
+    a.gemm(p.id, "check", C + (8 << 20), bad_A, B, M, N, 256, 256, 256, N)   # K = 256: the zero row grows
+    upload(C, np.full(M * N, 0x3F80, np.uint16))                          # C = 1.0 before the replay
+    gr.launch()
+    torch.cuda.synchronize()
+    assert not download(C, 2 * M * N).any()                                # zeros from the old zero row
+    assert a.device_flags() == 0
+    gr.close()

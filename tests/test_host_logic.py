@@ -219,6 +219,30 @@ def test_launch_validation_on_virtual_arena():
     assert e.value.status == g.GD_ERR_UNSUPPORTED                         # (valid; no device here)
 
 
+def test_per_access_flag_validation():
+    """GD_FENCE_PER_ACCESS is a flag OR-ed into the mode of any launch
+    (include/guardian.h): accepted with every mode, any other bit above the
+    mode byte or a mode past CLAMP is INVALID_ARG, before anything runs."""
+    a = virtual()
+    p = a.partition_alloc(1 << 20)
+    for m in ("none", "mask", "check", "modulo", "maskcount", "clamp"):
+        with pytest.raises(g.GuardianError) as e:                       # valid; no device here
+            a.copy(p.id, m + "+pa", p.base, p.base + 16, 64)
+        assert e.value.status == g.GD_ERR_UNSUPPORTED
+        assert g._mode(m + "+pa") == g.MODES[m] | g.GD_FENCE_PER_ACCESS
+    for bad in (g.GD_MODE_CHECK | 0x200, g.GD_MODE_CHECK | 0x10000, 6 | g.GD_FENCE_PER_ACCESS, 0xFF):
+        with pytest.raises(g.GuardianError) as e:
+            a.copy(p.id, bad, p.base, p.base + 16, 64)
+        assert e.value.status == g.GD_ERR_INVALID_ARG
+    with pytest.raises(ValueError):
+        g._mode("check+xx")
+    items = [g.work(p.id, g.GD_KIND_COPY, "check+pa", ptr=(p.base, p.base + 64), u64=(64,)),
+             g.work(p.id, g.GD_KIND_COPY, g.GD_MODE_MASK | 0x400, ptr=(p.base, p.base + 64), u64=(64,))]
+    with pytest.raises(g.GuardianError) as e:                            # launcher: bad flag found first
+        a.launcher_run(items, [None])
+    assert e.value.status == g.GD_ERR_INVALID_ARG
+
+
 def test_arena_wrap_errors():
     st, _ = g.gd_arena_wrap(-1, DEV_BASE, 3 << 20)
     assert st == g.GD_ERR_NOT_POW2
