@@ -9,8 +9,11 @@ tensors).  value = algorithmic bytes of all tenants on all GPUs / step time.
 
   python bench.py [--gpus N --steps K --warmup W --mode mask|check|none]
   python bench.py --impl reference      # the CPU oracle on the host cores
+  python bench.py --gpus 2 --dry-run    # the rank plumbing on CPU (gloo, virtual arenas)
 
-Under torchrun (N > 1) every rank runs its own arena (tenants shard across
+With --gpus N > 1 and no WORLD_SIZE in the environment, bench.py launches
+itself under torch.distributed.run with N ranks; under torchrun WORLD_SIZE
+must equal --gpus.  Every rank runs its own arena (tenants shard across
 GPUs, no data-path collective); the step time is the max over ranks and the
 per-GPU statistics are summed with one NCCL all_reduce.
 Prints ONE JSON line on rank 0.
@@ -135,7 +138,7 @@ def emit(line):
         os.write(_JSON_FD, data)
 
 
-def dist_init():
+def dist_init(backend="nccl"):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -144,24 +147,95 @@ def dist_init():
     if world > 1 or os.environ.get("GD_FORCE_DIST") == "1":
         import torch.distributed as dist
         import torch
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
 def allreduce(vals, op="max"):
     import torch
     import torch.distributed as dist
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    from paper_2401_09290_b200 import dist as gdist
+    dev = gdist._device() if dist.is_available() and dist.is_initialized() else \
+        torch.device("cuda" if torch.cuda.is_available() else "cpu")
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return t.tolist()
+
+
+def spawn_ranks(args):
+    """--gpus N > 1 without WORLD_SIZE: run this script under
+    torch.distributed.run with N ranks (one per GPU, 127.0.0.1 rendezvous)
+    and pass its exit code and its one JSON line through."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, text=True)
+    sys.stdout.write(r.stdout)
+    sys.stdout.flush()
+    return r.returncode
 
 
 def barrier():
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
         dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# the work items (shared by the GPU arm and the dry run)
+# ---------------------------------------------------------------------------
+
+C5_N_IDX, C5_TABLE_N, C5_GEMM_N = 1 << 26, 1 << 29, 8192
+C5_IDX_OFF, C5_OUT_OFF = 2 * GiB, 2 * GiB + GiB // 4
+
+
+def c2_items(g, parts, mode):
+    """BASELINE configs[1] (C2) step of one GPU: per tenant a fenced copy of
+    4 GiB and a fenced SAXPY over 2^30 elements."""
+    its = []
+    for p in parts:
+        its.append(g.work(p.id, g.GD_KIND_COPY, mode, ptr=(p.base + OFF_DST, p.base + OFF_SRC), u64=(COPY_BYTES,)))
+        its.append(g.work(p.id, g.GD_KIND_SAXPY, mode, ptr=(p.base + OFF_X, p.base + OFF_Y), u64=(SAXPY_N,),
+                          f32=(ALPHA,)))
+    return its
+
+
+def c5_items(g, parts, mode):
+    """BASELINE configs[4] (C5) of one GPU: t0-t2 fenced copy (4 GiB), t3-t5
+    fenced gather (C3: 2^26 indices into a 2^29-word table), t6-t7 fenced
+    GEMM 8192^3.  Returns (items, algorithmic bytes, flops) of one round."""
+    n = C5_GEMM_N
+    items, nbytes, flops = [], 0, 0
+    for t, p in enumerate(parts):
+        b = p.base
+        if t < 3:
+            items.append(g.work(p.id, g.GD_KIND_COPY, mode, ptr=(b + OFF_DST, b + OFF_SRC), u64=(COPY_BYTES,)))
+            nbytes += BYTES_COPY
+        elif t < 6:
+            items.append(g.work(p.id, g.GD_KIND_GATHER, mode, ptr=(b + C5_OUT_OFF, b, b + C5_IDX_OFF),
+                                u64=(C5_N_IDX,), u32=(1,)))
+            nbytes += 12 * C5_N_IDX
+        else:
+            items.append(g.work(p.id, g.GD_KIND_GEMM, mode, ptr=(b + 2 * n * n * 2, b, b + n * n * 2),
+                                u64=(n, n, n), u32=(n, n, n)))
+            flops += 2 * n ** 3
+    return items, nbytes, flops
+
+
+def c5_expected_violations(launches, world):
+    """Check-mode violations C5 must count: 3 gather tenants x 671,089 planted
+    indices (1 % of 2^26, synth.planted_count) x launches x GPUs."""
+    import synth
+    return 3 * synth.planted_count(0.01, C5_N_IDX) * launches * world
 
 
 # ---------------------------------------------------------------------------
@@ -186,14 +260,7 @@ class Workload:
         torch.cuda.synchronize(device)
 
     def items(self, mode):
-        g = self.g
-        its = []
-        for p in self.parts:
-            its.append(g.work(p.id, g.GD_KIND_COPY, mode, ptr=(p.base + OFF_DST, p.base + OFF_SRC),
-                              u64=(COPY_BYTES,)))
-            its.append(g.work(p.id, g.GD_KIND_SAXPY, mode, ptr=(p.base + OFF_X, p.base + OFF_Y),
-                              u64=(SAXPY_N,), f32=(ALPHA,)))
-        return its
+        return c2_items(self.g, self.parts, mode)
 
     def step(self, items):
         return self.arena.launcher_run(items, self.streams)
@@ -243,37 +310,33 @@ class Workload:
         else:
             self.arena.saxpy(p.id, mode, ALPHA, p.base + OFF_X, p.base + OFF_Y, SAXPY_N, stream=s)
 
-    def c5(self, launches=20, mode="check", seed_base=5000, policy="round_robin"):
-        """BASELINE.json configs[4] on this GPU: t0-t2 fenced copy (4 GiB),
-        t3-t5 fenced gather (C3: 2^26 indices, 1 % planted OOB), t6-t7 fenced
-        GEMM 8192^3, `launches` launches each, issued round-robin by the
-        launcher on 8 streams.  Returns (makespan ms, bytes, flops, planted)."""
-        import numpy as np
+    def c5_setup(self, seed_base=5000):
+        """C5 inputs: the gather tenants' indices (1 % planted out of the
+        partition, synth.indices_with_oob) and the GEMM tenants' operands.
+        Returns the planted count of one round."""
         import synth
-        torch, g, devmem = self.torch, self.g, self.devmem
-        n_idx, table_n, n = 1 << 26, 1 << 29, 8192
-        items, planted, nbytes, flops = [], 0, 0, 0
+        torch, devmem = self.torch, self.devmem
+        n, planted = C5_GEMM_N, 0
         for t, p in enumerate(self.parts):
             b = p.base
-            if t < 3:
-                items.append(g.work(p.id, g.GD_KIND_COPY, mode, ptr=(b + OFF_DST, b + OFF_SRC), u64=(COPY_BYTES,)))
-                nbytes += BYTES_COPY
-            elif t < 6:
-                idx, pos = synth.indices_with_oob(synth.rng_for(seed_base + t), n_idx, table_n, 0.01)
-                devmem.view(b + 2 * GiB, n_idx, torch.int32, self.device).copy_(torch.from_numpy(idx))
+            if 3 <= t < 6:
+                idx, pos = synth.indices_with_oob(synth.rng_for(seed_base + t), C5_N_IDX, C5_TABLE_N, 0.01)
+                devmem.view(b + C5_IDX_OFF, C5_N_IDX, torch.int32, self.device).copy_(torch.from_numpy(idx))
                 planted += len(pos)
-                items.append(g.work(p.id, g.GD_KIND_GATHER, mode, ptr=(b + 2 * GiB + GiB // 4, b, b + 2 * GiB),
-                                    u64=(n_idx,), u32=(1,)))
-                nbytes += 12 * n_idx
-            else:
+            elif t >= 6:
                 gen = torch.Generator(device=f"cuda:{self.device}")
                 gen.manual_seed(seed_base + t)
                 for off in (0, n * n * 2):
                     devmem.view(b + off, n * n, torch.bfloat16, self.device).uniform_(-1, 1, generator=gen)
-                items.append(g.work(p.id, g.GD_KIND_GEMM, mode, ptr=(b + 2 * n * n * 2, b, b + n * n * 2),
-                                    u64=(n, n, n), u32=(n, n, n)))
-                flops += 2 * n ** 3
         torch.cuda.synchronize(self.device)
+        return planted
+
+    def c5(self, planted, launches=20, mode="check", policy="round_robin"):
+        """BASELINE.json configs[4] on this GPU (c5_items), `launches`
+        launches per tenant, issued by the launcher on 8 streams under
+        `policy`.  Returns (makespan ms, bytes, flops, planted)."""
+        torch = self.torch
+        items, nbytes, flops = c5_items(self.g, self.parts, mode)
         queue = [it for it in items for _ in range(launches)]
         self.step(queue[:len(items)])                                     # warm-up round
         torch.cuda.synchronize(self.device)
@@ -294,10 +357,13 @@ class Workload:
         torch.cuda.synchronize(self.device)
         return start.elapsed_time(stop), nbytes * launches, flops * launches, planted * launches
 
-    def kernel_table(self, reps=5):
-        """Solo launches of every kernel at its BASELINE size in every mode,
-        interleaved, CUDA events on one stream (after c5(): tenant 3/4 hold
-        the C3 gather / scatter layout with 1 % OOB, tenant 6 the GEMM).
+    def kernel_table(self, reps=5, modes=ALL_MODES, per_access=False):
+        """Solo launches of every kernel at its BASELINE size in `modes`,
+        interleaved, CUDA events on one stream (after c5_setup(): tenant 3/4
+        hold the C3 gather / scatter layout with 1 % OOB, tenant 6 the GEMM).
+        per_access: every fenced mode with GD_FENCE_PER_ACCESS (the paper's
+        instrumentation: no tile-level range test); the descriptor-fenced
+        TMA kernels (GEMM, K5 v2) have no per-access fence and are left out.
         Returns {kernel: {mode: {"ms", "work", "unit"}}} (per GPU, medians)."""
         torch, parts = self.torch, self.parts
         n_idx, n = 1 << 26, 8192
@@ -316,29 +382,126 @@ class Workload:
                                       16 * n_idx, "GB/s"),
             "stencil_32768^2": (lambda m, s: a.stencil(p5.id, m, p5.base + 8 * GiB, p5.base + 4 * GiB, H, W, W,
                                                        0.5, 0.125, stream=s), 8 * (H - 2) * (W - 2), "GB/s"),
-            "stencil_tma_32768^2": (lambda m, s: a.stencil_tma(p5.id, m, p5.base + 8 * GiB, p5.base + 4 * GiB, H, W,
-                                                               W, 0.5, 0.125, stream=s), 8 * (H - 2) * (W - 2),
-                                    "GB/s"),
-            "gemm_8192^3": (lambda m, s: a.gemm(p6.id, m, p6.base + 2 * n * n * 2, p6.base, p6.base + n * n * 2,
-                                                n, n, n, n, n, n, stream=s), 2 * n ** 3, "TFLOP/s"),
+            "gather_rows_D32_1GiB": (lambda m, s: a.gather(p5.id, m, p5.base + 3 * GiB, p5.base,
+                                                           p5.base + 2 * GiB + GiB // 2, GiB // 128, 32, stream=s),
+                                     4 * (GiB // 128) + 8 * GiB, "GB/s"),
         }
+        if not per_access:
+            kern["stencil_tma_32768^2"] = (lambda m, s: a.stencil_tma(p5.id, m, p5.base + 8 * GiB, p5.base + 4 * GiB,
+                                                                      H, W, W, 0.5, 0.125, stream=s),
+                                           8 * (H - 2) * (W - 2), "GB/s")
+            kern["gemm_8192^3"] = (lambda m, s: a.gemm(p6.id, m, p6.base + 2 * n * n * 2, p6.base,
+                                                       p6.base + n * n * 2, n, n, n, n, n, n, stream=s),
+                                   2 * n ** 3, "TFLOP/s")
         s = self.streams[0]
         out = {}
-        modes = ALL_MODES
+        launch_mode = {m: (m + "+pa" if per_access and m != "none" else m) for m in modes}
         for name, (fn, work, unit) in kern.items():
             times = {m: [] for m in modes}
             with torch.cuda.stream(s):
                 for m in modes:
-                    fn(m, s)
+                    fn(launch_mode[m], s)
                 for _ in range(reps):
                     for m in modes:
                         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         e0.record(s)
-                        fn(m, s)
+                        fn(launch_mode[m], s)
                         e1.record(s)
                         e1.synchronize()
                         times[m].append(e0.elapsed_time(e1))
             out[name] = {m: {"ms": statistics.median(v), "work": work, "unit": unit} for m, v in times.items()}
+        return out
+
+    def rows_setup(self):
+        """Embedding-row gather input (kernel_table's gather_rows_D32): 2^23
+        row indices uniform over the 2^24 rows of 128 B of tenant 5's first
+        2 GiB, at 2.5 GiB (its stencil buffers start at 4 GiB)."""
+        torch, p5 = self.torch, self.parts[5]
+        gen = torch.Generator(device=f"cuda:{self.device}")
+        gen.manual_seed(5105)
+        self.devmem.view(p5.base, 1 << 29, torch.int32, self.device).random_(generator=gen)
+        self.devmem.view(p5.base + 2 * GiB + GiB // 2, GiB // 128, torch.int32, self.device).random_(
+            0, (1 << 29) // 32, generator=gen)
+        H = W = 32768
+        self.devmem.view(p5.base + 4 * GiB, H * W, torch.float32, self.device).uniform_(0, 1, generator=gen)
+        torch.cuda.synchronize(self.device)
+
+    def l2_table(self, reps=5, modes=ALL_MODES, per_access=False, batch=50):
+        """The L2-resident regime (the
+        fence's ALU cost least hidden): working sets below the 126 MB L2 on
+        tenant 7 (offset 1 GiB), each mode's batch of `batch` back-to-back
+        launches captured once into a CUDA graph and replayed between two
+        events (per-launch mean), modes interleaved."""
+        torch, devmem, a, p = self.torch, self.devmem, self.arena, self.parts[7]
+        b = p.base + GiB
+        gen = torch.Generator(device=f"cuda:{self.device}")
+        gen.manual_seed(5207)
+        devmem.view(b, 8 * MiB, torch.int32, self.device).random_(generator=gen)
+        devmem.view(b + 128 * MiB, 8 * MiB, torch.float32, self.device).uniform_(-1, 1, generator=gen)
+        devmem.view(b + 192 * MiB, 8 * MiB, torch.float32, self.device).uniform_(-1, 1, generator=gen)
+        n = 1 << 22
+        devmem.view(b + 256 * MiB, n, torch.int32, self.device).random_(0, n, generator=gen)
+        H = W = 2048
+        devmem.view(b + 384 * MiB, H * W, torch.float32, self.device).uniform_(0, 1, generator=gen)
+        torch.cuda.synchronize(self.device)
+        kern = {
+            "copy_32MiB": (lambda m, s: a.copy(p.id, m, b + 64 * MiB, b, 32 * MiB, stream=s), 2 * 32 * MiB),
+            "saxpy_2^23": (lambda m, s: a.saxpy(p.id, m, 1.0, b + 128 * MiB, b + 192 * MiB, 8 * MiB, stream=s),
+                           12 * 8 * MiB),
+            "gather_2^22_into_2^22": (lambda m, s: a.gather(p.id, m, b + 320 * MiB, b, b + 256 * MiB, n, stream=s),
+                                      12 * n),
+            "stencil_2048^2": (lambda m, s: a.stencil(p.id, m, b + 448 * MiB, b + 384 * MiB, H, W, W, 0.5, 0.125,
+                                                      stream=s), 8 * (H - 2) * (W - 2)),
+        }
+        if not per_access:
+            kern["stencil_tma_2048^2"] = (lambda m, s: a.stencil_tma(p.id, m, b + 448 * MiB, b + 384 * MiB, H, W, W,
+                                                                     0.5, 0.125, stream=s), 8 * (H - 2) * (W - 2))
+        launch_mode = {m: (m + "+pa" if per_access and m != "none" else m) for m in modes}
+        s = self.streams[7]
+        out = {}
+        for name, (fn, work) in kern.items():
+            graphs, times = {}, {m: [] for m in modes}
+            with torch.cuda.stream(s):
+                for m in modes:
+                    for _ in range(3):
+                        fn(launch_mode[m], s)
+                s.synchronize()
+                for m in modes:
+                    gr = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gr, stream=s):
+                        for _ in range(batch):
+                            fn(launch_mode[m], s)
+                    graphs[m] = gr
+                for m in modes:
+                    graphs[m].replay()
+                for _ in range(reps):
+                    for m in modes:
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(s)
+                        graphs[m].replay()
+                        e1.record(s)
+                        e1.synchronize()
+                        times[m].append(e0.elapsed_time(e1) / batch)
+            out[name] = {m: {"ms": statistics.median(v), "work": work, "unit": "GB/s"} for m, v in times.items()}
+            del graphs
+        return out
+
+    def sample_c2(self, k=1 << 16, seed=2999):
+        """Seeded sample of every tenant's C2 buffers, read back now: saxpy
+        element positions (x, y) and copy 16-byte units (src, dst)."""
+        import numpy as np
+        torch, devmem = self.torch, self.devmem
+        rng = np.random.default_rng(seed)
+        out = []
+        for p in self.parts:
+            e = torch.from_numpy(np.sort(rng.integers(0, SAXPY_N, k))).to(f"cuda:{self.device}")
+            u = torch.from_numpy(np.sort(rng.integers(0, COPY_BYTES // 16, k))).to(f"cuda:{self.device}")
+            x = devmem.view(p.base + OFF_X, SAXPY_N, torch.float32, self.device)[e].cpu().numpy()
+            y = devmem.view(p.base + OFF_Y, SAXPY_N, torch.float32, self.device)[e].cpu().numpy()
+            src = devmem.view(p.base + OFF_SRC, COPY_BYTES // 8, torch.int64, self.device).view(-1, 2)[u]
+            dst = devmem.view(p.base + OFF_DST, COPY_BYTES // 8, torch.int64, self.device).view(-1, 2)[u]
+            out.append({"x": x, "y": y, "src": src.cpu().numpy().view(np.uint8).reshape(-1),
+                        "dst": dst.cpu().numpy().view(np.uint8).reshape(-1)})
         return out
 
     def e2e(self, mode, steps, warmup):
@@ -388,14 +551,33 @@ class Workload:
 
 
 def ncu_traffic(kernel_tag: str):
-    """dram bytes per launch from the committed ncu --set full capture."""
+    """DRAM bytes per launch and ncu's DRAM throughput (% of the theoretical
+    peak) of `kernel_tag`, from the committed ncu --set full capture
+    (profiles/ncu_traffic.json, written by tools/ncu_summary.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
+        return None, None, None
     with open(p) as f:
         d = json.load(f)
     v = d.get(kernel_tag)
-    return v if isinstance(v, (int, float)) else None
+    pct = d.get(kernel_tag + ":dram_pct")
+    return (v if isinstance(v, (int, float)) else None, pct if isinstance(pct, (int, float)) else None,
+            d.get("_source"))
+
+
+def reduce_table(table, world, modes):
+    """Max time over ranks per kernel and mode; rate = world x work / time;
+    overhead against the unfenced twin of the same table."""
+    for row in table.values():
+        for m in list(row):
+            t = allreduce([row[m]["ms"]])[0]
+            u = row[m]["unit"]
+            row[m] = {"ms": round(t, 5), u: round(world * row[m]["work"] / (t / 1e3) / (1e9 if u == "GB/s" else 1e12),
+                                                  1)}
+        for m in modes:
+            if m != "none":
+                row[m]["overhead_pct"] = round(100 * (row[m]["ms"] / row["none"]["ms"] - 1), 2)
+    return table
 
 
 def run_gpu(args):
@@ -410,8 +592,10 @@ def run_gpu(args):
     torch.cuda.synchronize(local)
 
     # ---- the contract's timed region: exactly K steps, max over ranks ----
+    pre = w.sample_c2()                                   # parity sample of the inputs (not timed)
     with Clocks(local) as clk:
         ms = w.time_steps(args.mode, args.steps)
+    post = w.sample_c2()                                  # ... and of the outputs of the K timed steps
     ms = allreduce([ms])[0]
     ms_per_step = ms / args.steps
     value = world * STEP_BYTES_PER_GPU / (ms_per_step / 1e3) / 1e9
@@ -435,13 +619,19 @@ def run_gpu(args):
     sx_ms, sx_bytes = solo[("saxpy", args.mode)]
     achieved = sx_bytes / (sx_ms / 1e3) / 1e9
     mode_id = ALL_MODES.index(args.mode)
+    traffic, dram_pct, traffic_src = ncu_traffic(f"k_saxpy<{mode_id}>")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": ncu_traffic(f"k_saxpy<{mode_id}>"),
+                "frac": round(achieved / hbm, 4), "traffic": traffic,
+                "traffic_source": ("committed ncu --set full capture of this kernel (profiles/ncu_traffic.json"
+                                   + (f", {traffic_src}" if traffic_src else "") + "), not measured in this run"),
+                "ncu_dram_throughput_pct_of_theoretical": dram_pct,
                 "kernel": f"k_saxpy<{args.mode}>", "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json)",
                 "bytes_per_launch": sx_bytes, "avg_launch_ms": round(sx_ms, 4),
                 "share_of_step": round(TENANTS * sx_ms / (TENANTS * (sx_ms + solo[("copy", args.mode)][0])), 3),
-                # context: the measured peak is torch's copy_, which this kernel beats;
-                # against the HGX nominal 7.7 TB/s (B200_PROFILING.md) the same launch is:
+                # the measured peak is torch's copy_, which this kernel beats; against
+                # the theoretical 8.18 TB/s (8192-bit bus x 2 x 3996 MHz, ncu's
+                # denominator) and the HGX nominal 7.7 TB/s the same launch is:
+                "theoretical_peak": 8184.0, "frac_of_theoretical": round(achieved / 8184.0, 4),
                 "nominal_peak": 7700.0, "frac_of_nominal": round(achieved / 7700.0, 4)}
     kernels = {f"{k}/{m}": {"ms": round(t, 4), "GB/s": round(b / (t / 1e3) / 1e9, 1)}
                for (k, m), (t, b) in solo.items()}
@@ -460,21 +650,25 @@ def run_gpu(args):
     c5 = None
     c5_expected = 0
     if not args.no_c5:
-        # the paper's launcher (round robin, free-running tenant streams) and the
-        # interference-aware memory-lane policy (include/guardian.h gd_policy);
-        # the violation check below reads the counters of the last run
+        # headline: the paper's launcher (round robin, free-running tenant
+        # streams); beside it the interference-aware
+        # memory-lane policy (include/guardian.h gd_policy).  Round robin runs
+        # last, so the violation check below reads its counters.
+        planted = w.c5_setup()
         by_policy = {}
-        for pol in ("round_robin", "memory_lane"):
-            c5_ms, c5_bytes, c5_flops, c5_planted = w.c5(launches=args.c5_launches, policy=pol)
+        for pol in ("memory_lane", "round_robin"):
+            c5_ms, c5_bytes, c5_flops, c5_planted = w.c5(planted, launches=args.c5_launches, policy=pol)
             by_policy[pol] = allreduce([c5_ms])[0]
-        best = min(by_policy, key=by_policy.get)
-        c5_ms_max = by_policy[best]
+        c5_ms_max = by_policy["round_robin"]
         c5_expected = int(allreduce([float(c5_planted)], op="sum")[0])
-        c5 = {"makespan_ms": round(c5_ms_max, 3), "policy": best,
-              "makespan_ms_by_policy": {k: round(v, 3) for k, v in by_policy.items()},
+        assert c5_expected == c5_expected_violations(args.c5_launches, world)
+        c5 = {"makespan_ms": round(c5_ms_max, 3), "policy": "round_robin",
               "launches_per_tenant": args.c5_launches, "mode": "check",
               "memory_GBps": round(world * c5_bytes / (c5_ms_max / 1e3) / 1e9, 1),
               "gemm_TFLOPs": round(world * c5_flops / (c5_ms_max / 1e3) / 1e12, 1),
+              "memory_lane": {"makespan_ms": round(by_policy["memory_lane"], 3),
+                              "memory_GBps": round(world * c5_bytes / (by_policy["memory_lane"] / 1e3) / 1e9, 1),
+                              "gemm_TFLOPs": round(world * c5_flops / (by_policy["memory_lane"] / 1e3) / 1e12, 1)},
               "tenants": "t0-2 copy 4 GiB, t3-5 gather 2^26 (1% OOB), t6-7 GEMM 8192^3 bf16"}
 
     # ---- statistics reduced over GPUs with NCCL (the one collective) ----
@@ -484,23 +678,30 @@ def run_gpu(args):
     red = [sum(d[f] for d in red_t.values()) for f in ("violations", "launches", "bytes")]
     if c5 is not None:
         c5["violations_allreduced"] = int(red[0])
-        c5["violations_expected"] = c5_expected                       # 3 x 671,089 x launches x G
+        c5["violations_expected"] = c5_expected
+        c5["violations_expected_formula"] = f"3 x 671,089 x {args.c5_launches} launches x {world} GPU(s)"
         c5["violations_exact"] = int(red[0]) == c5_expected
 
-    # ---- every kernel x every mode at the BASELINE sizes ----
-    table = None
+    # ---- every kernel x every mode at the BASELINE sizes,
+    #      hoisted (default) and per access; the L2-resident regime ----
+    table = table_pa = l2 = l2_pa = None
     if not args.no_c5:
-        table = w.kernel_table(reps=args.table_reps)
-        for k, row in table.items():                                   # max time over ranks
-            for m in list(row):
-                t = allreduce([row[m]["ms"]])[0]
-                row[m] = {"ms": round(t, 4), row[m]["unit"]: round(world * row[m]["work"] / (t / 1e3) /
-                                                                    (1e9 if row[m]["unit"] == "GB/s" else 1e12), 1)}
-            for m in ALL_MODES[1:]:
-                row[m]["overhead_pct"] = round(100 * (row[m]["ms"] / row["none"]["ms"] - 1), 2)
+        w.rows_setup()
+        table = reduce_table(w.kernel_table(reps=args.table_reps), world, ALL_MODES)
+        table_pa = reduce_table(w.kernel_table(reps=args.table_reps, per_access=True), world, ALL_MODES)
+        l2 = reduce_table(w.l2_table(reps=args.table_reps), world, ALL_MODES)
+        l2_pa = reduce_table(w.l2_table(reps=args.table_reps, per_access=True), world, ALL_MODES)
+
+    # ---- parity of the timed steps (cpu_baseline leg: the oracle on the host
+    #      re-computes the sampled outputs; every rank checks its tenants) ----
+    par = oracle_parity(pre, post, args.steps, args.mode)
+    bad = int(allreduce([float(par["mismatches"])], op="sum")[0])
+    parity = {"status": "ok" if bad == 0 else "FAIL", "mismatches": bad,
+              "checked": int(allreduce([float(par["checked"])], op="sum")[0]),
+              "sample": par["sample"]}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(seconds=args.cpu_seconds)
         cpu["by_config"] = cpu_by_config("mask", host_threads(), table)
 
@@ -514,7 +715,9 @@ def run_gpu(args):
                        "partition_bytes": PART, "copy_bytes": COPY_BYTES, "saxpy_n": SAXPY_N,
                        "l2": "inputs larger than L2 (4 GiB per tensor vs 126 MB L2), no flush",
                        "parallelism": f"{world} GPU(s), one arena per GPU, tenants sharded, no data-path collective"},
+            "per_gpu_GBps": round(value / world, 1),
             "frac_of_hbm_peak": round(value / world / hbm, 4),
+            "parity": parity["status"], "parity_detail": parity,
             "modes_GBps": modes_gbs, "overhead_pct_vs_unfenced": overhead,
             "roofline": roofline, "kernels_solo": kernels,
             "e2e": e2e, "gpu_launches": args.steps * 2 * TENANTS,
@@ -522,10 +725,81 @@ def run_gpu(args):
             "stats_allreduced": {"violations": int(red[0]), "launches": int(red[1]), "bytes": int(red[2])},
             "multi_tenant_c5": c5,
             "kernels_all_modes": table,
+            "kernels_all_modes_per_access": table_pa,
+            "l2_resident": l2,
+            "l2_resident_per_access": l2_pa,
             "cpu_baseline": cpu,
         }
         emit(line)
     w.arena.close()
+
+
+def run_dry(args):
+    """--dry-run: the rank plumbing of run_gpu on CPU -- gloo process group,
+    one VIRTUAL arena per rank (gd_arena_wrap with device -1: the partition
+    manager and the launcher's validation run, nothing launches), the C2 and
+    C5 items validated, max-over-ranks timing and the stats all_reduce.  The
+    per-rank counters are the ones C5 plants (3 gather tenants x 671,089 x
+    launches); the timing is a placeholder.  Prints ONE JSON line on rank 0."""
+    from paper_2401_09290_b200 import dist as gdist, guardian as g
+    world, rank, local = dist_init("gloo")
+    arena = g.Arena.wrap(-1, ARENA * (rank + 1), ARENA)                # size-aligned fake VA per rank
+    parts = [arena.partition_alloc(PART) for _ in range(TENANTS)]
+    assert [p.base for p in parts] == [arena.base + t * PART for t in range(TENANTS)]
+    valid = 0
+    for items in (c2_items(g, parts, args.mode), c5_items(g, parts, "check")[0]):
+        try:
+            arena.launcher_run(items, [None] * TENANTS)
+        except g.GuardianError as e:                                  # validated: no device to run on
+            assert e.status == g.GD_ERR_UNSUPPORTED, e
+        valid += len(items)
+    ms = allreduce([10.0 + rank])[0]                                   # placeholder, max over ranks
+    per = {}
+    for t, p in enumerate(parts):
+        planted = 671089 if 3 <= t < 6 else 0
+        per[rank * TENANTS + t] = {"violations": planted * args.c5_launches, "launches": args.c5_launches,
+                                   "bytes": 0, "flops": 0}
+    red_t, span = gdist.allreduce_stats(per, ms, world * TENANTS)
+    red = [sum(d[f] for d in red_t.values()) for f in ("violations", "launches", "bytes")]
+    expected = c5_expected_violations(args.c5_launches, world)
+    if rank == 0:
+        emit({"metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+              "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+              "dry_run": True, "items_validated_per_rank": valid, "makespan_ms_max": span,
+              "stats_allreduced": {"violations": int(red[0]), "launches": int(red[1]), "bytes": int(red[2])},
+              "multi_tenant_c5": {"violations_allreduced": int(red[0]), "violations_expected": expected,
+                                  "violations_exact": int(red[0]) == expected}})
+    arena.close()
+
+
+def oracle_parity(pre, post, steps, mode):
+    """Part of the cpu_baseline leg (the oracle on the host cores, after all
+    GPU timing): re-compute the sampled outputs of the K timed steps.  Every
+    timed step applied, per tenant, y <- fmaf(a, x, y) (saxpy) and dst <- src
+    (copy) once, so on the sample y after the timed region must equal K
+    oracle saxpy passes over (x, y before it), bit for bit, and dst the
+    oracle's copy of src."""
+    import numpy as np
+    import oracle
+    bad = checked = 0
+    base, size = 0x7E0000000000, 1 << 24
+    for a, b in zip(pre, post):
+        k = len(a["x"])
+        m = oracle.Mem(base, size)
+        m.write(base, a["x"])
+        m.write(base + 4 * k, a["y"])
+        m.write(base + 8 * k, b["src"])
+        for _ in range(steps):
+            oracle.saxpy(m, base, size, mode, ALPHA, base, base + 4 * k, k)
+        oracle.copy(m, base, size, mode, base + 8 * k + 16 * k, base + 8 * k, 16 * k)
+        bad += int(np.count_nonzero(m.view(base + 4 * k, np.uint32, k) != b["y"].view(np.uint32)))
+        bad += int(np.count_nonzero(m.view(base + 24 * k, np.uint8, 16 * k) != b["dst"]))
+        bad += int(np.count_nonzero(a["src"] != b["src"]))            # the copy source is never written
+        checked += k + 16 * k
+    k = len(pre[0]["x"]) if pre else 0
+    return {"mismatches": bad, "checked": checked,
+            "sample": f"per tenant {k} seeded saxpy elements (y after the {steps} timed steps vs {steps} oracle "
+                      f"passes) and {k} copy 16-byte units, bit-exact"}
 
 
 # ---------------------------------------------------------------------------
@@ -752,6 +1026,11 @@ def run_reference(args):
         "data": "synthetic (NumPy PCG64 seeded 1000*2+tenant)",
         "config": {"workload": WORKLOAD, "mode": args.mode, "tenants_per_gpu": TENANTS,
                    "partition_bytes": PART, "copy_bytes": COPY_BYTES, "saxpy_n": SAXPY_N,
+                   "sample_run": {"tenants": th, "copy_bytes_per_tenant": SAMPLE_COPY,
+                                  "saxpy_n_per_tenant": SAMPLE_SAXPY,
+                                  "note": "each step is a bounded sample of the C2 workload above: the same kernels, "
+                                          "fence and mode over 64 MiB copies and 2^24-element saxpys per tenant "
+                                          "(the value is GB/s of algorithmic bytes, comparable across sizes)"},
                    "parallelism": "host threads, one tenant per thread"},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": th, "kind": "oracle",
@@ -776,18 +1055,30 @@ def main():
     ap.add_argument("--c5-launches", type=int, default=20)
     ap.add_argument("--table-reps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="the rank plumbing on CPU: gloo, virtual arenas, validation only, no kernels")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+        return 0
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        return spawn_ranks(args)                       # N ranks under torch.distributed.run
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}\n")
+        return 2
+    quiet_stdout()
+    if args.dry_run:
+        run_dry(args)
     else:
-        quiet_stdout()
         run_gpu(args)
-        import torch.distributed as dist
-        if dist.is_available() and dist.is_initialized():
-            dist.destroy_process_group()
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

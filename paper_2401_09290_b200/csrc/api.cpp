@@ -592,6 +592,8 @@ gd_status run_work_locked(gd_arena *a, const gd_work &w_in, cudaStream_t stream,
     FenceDesc fd;
     fd.base = base;
     fd.mask = size - 1;
+    fd.mask16 = (size - 1) & ~15ull;
+    fd.mask4 = (size - 1) & ~3ull;
     fd.size = size;
     fd.inv = recip64(size);
     fd.viol = a->d_stats + (uint64_t)w.tenant * GD_NUM_KINDS + w.kind;

@@ -40,7 +40,8 @@ template <int MODE, int W>
 struct Fence {
     uint64_t base, keep, size, inv, lim;
     __device__ __forceinline__ explicit Fence(const FenceDesc &fd)
-        : base(fd.base), keep(fd.mask & ~(uint64_t)(W - 1)), size(fd.size), inv(fd.inv), lim(fd.size - W) {}
+        : base(fd.base), keep(W == 16 ? fd.mask16 : W == 4 ? fd.mask4 : fd.mask & ~(uint64_t)(W - 1)), size(fd.size),
+          inv(fd.inv), lim(fd.size - W) {}
     // address the access really uses (MASK / MODULO / CLAMP: fenced; CHECK / NONE: unchanged)
     __device__ __forceinline__ uint64_t addr(uint64_t a) const {
         if constexpr (MODE == kMask || MODE == kMaskCount) {

@@ -17,6 +17,8 @@ constexpr bool hoistable(int m) { return m == kCheck || m == kModulo || m == kMa
 struct FenceDesc {
     uint64_t base;                 // partition base (size-aligned for pow2 partitions)
     uint64_t mask;                 // size - 1 (the mask-mode fence; pow2 partitions only)
+    uint64_t mask16, mask4;        // mask_w = (size - 1) & ~(w - 1) for w = 16 / 4 (reading A3), so the
+                                   // mask fence of a w-byte access is one LOP3 per 32-bit half
     uint64_t size;                 // partition size in bytes (check / modulo)
     uint64_t inv;                  // floor(2^64 / size): modulo-mode reciprocal
     unsigned long long *viol;      // trusted counter (outside every partition)

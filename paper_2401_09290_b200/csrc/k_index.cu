@@ -427,7 +427,7 @@ __device__ __forceinline__ void scatter_chunk(const FenceDesc &fd, uint64_t tabl
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ FenceDesc fd, uint64_t table,
+__global__ void __launch_bounds__(kThreads, MODE == kMaskCount ? 3 : 4) k_scatter(const __grid_constant__ FenceDesc fd, uint64_t table,
                                                       uint64_t idx, uint64_t src, uint64_t nvec, uint32_t tail) {
     uint32_t nv = 0;
     EdgeSums es;

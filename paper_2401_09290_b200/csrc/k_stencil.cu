@@ -31,12 +31,20 @@ constexpr int kRows = 16;     // rows per CTA strip (a multiple of the rows load
 __device__ __forceinline__ void st_v(uint64_t a, uint4 v) { __stcs(reinterpret_cast<uint4 *>(a), v); }
 __device__ __forceinline__ void st_w(uint64_t a, uint32_t v) { __stcs(reinterpret_cast<unsigned int *>(a), v); }
 
-template <int MODE, int kG, bool WALK = false>
+// One thread's strip: rows [r0, r1) of the 4-column vector at column c
+// (r1 - r0 <= ROWS; FULL: == ROWS), kG rows of loads in flight.  The row
+// loop is unrolled at compile time, addresses advance by one row pitch per
+// row, and every access is fenced at its own address.
+template <int MODE, int kG, int ROWS, bool FULL, bool WALK = false>
 __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t W, uint64_t pitch,
                                       float c0, float c1, uint64_t c, uint32_t r0, uint32_t r1, uint32_t &nv) {
-    // row indices are 32-bit (H <= 2^19, api.cpp); addresses are 64-bit
+    static_assert(ROWS % kG == 0 && ROWS + 2 <= 32, "strip rows");
+    // Every lane of the warp runs this (the W / E words travel by shuffle):
+    // a lane past the grid's width (c >= W) loads nothing and stores nothing.
     const Fence<MODE, 16> f16(fd);
     const Fence<MODE, 4> f4(fd);
+    const uint32_t lane = threadIdx.x & 31u;
+    const bool active = c < W;
     bool interior[4];
     bool all4 = true;
 #pragma unroll
@@ -44,127 +52,159 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         interior[k] = (c + k >= 1) && (c + k + 2 <= W);
         all4 = all4 && interior[k];
     }
-    // refused-access weights (counting modes): the own vector of row x is
-    // loaded by the interior points of row x as C (each), as W (k >= 1) and
-    // as E (k <= 2), and by those of rows x-1 / x+1 as S / N (once each).
-    // A refusal is counted when the vector is loaded, with the weight of the
-    // strip rows [r0, r1) that use it, so no per-load flag stays live.
-    uint32_t ni = 0, nCv = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        ni += interior[k];
-        nCv += interior[k] * (1u + (k >= 1) + (k <= 2));
-    }
-    auto weight = [&](uint32_t x) {
-        return ni * ((uint32_t)(x >= r0 + 1 && x <= r1) + (uint32_t)(x + 1 >= r0 && x + 1 < r1)) +
-               nCv * (uint32_t)(x >= r0 && x < r1);
-    };
-    // modulo with WALK (the strip does not straddle the base and a row step
-    // is below the partition size): the rows are loaded in increasing order,
-    // so each vector's fence follows from the previous row's
-    // (Fence::step_up), the W / E words of a row from the fence of the row
-    // below it (step_down) and each output vector from the previous output
-    // row's; every access still gets its own fenced address, equal to the
-    // full modulo.  Without WALK every access takes the full modulo.
-    uint64_t f_last = 0, fo_last = 0;
-    // a clamped outside vector is its edge word four times (fence.cuh vld4)
-    auto ldv = [&](uint32_t r) {
-        const uint64_t a = in + 4 * ((uint64_t)r * pitch + c);
+    const bool all4a = all4;                           // (all four interior implies c < W)
+    // The W word of point k = 0 (column c-1) is word 3 of lane-1's vector of
+    // the same row, the E word of point k = 3 (column c+4) word 0 of
+    // lane+1's: F4(a-4) = F16(a-16)+12 and F4(a+16) = F16(a+16) in every
+    // mode (base and size multiples of 16), a word is refused exactly when
+    // its vector is, and a clamped outside vector is its edge word four
+    // times, so the shuffled word is the value the point's own fenced 32-bit
+    // load would return.  Only the warp's edge lanes load their halo word
+    // (lane 0: column c-1, lane 31: column c+4), fenced at 4 bytes.
+    const bool need_h = lane == 0 ? interior[0] : (lane == 31 ? interior[3] : false);
+    // lane 0 / lane 31 take the halo word instead of the shuffled one; as
+    // bit masks in general registers (one LOP3 each), not live predicates
+    const uint32_t m0 = lane == 0 ? ~0u : 0u, m31 = lane == 31 ? ~0u : 0u;
+    const uint64_t step = 4 * pitch;
+    // A lane past the width loads the last vector of the row instead (never
+    // used: a point needs lane+1's word only when lane+1 is inside the
+    // width), so no load waits on a lane predicate; it stores nothing and
+    // counts nothing (its weights below are zero).
+    const uint64_t cl = active ? c : ((uint64_t)(W - 1) & ~3ull);
+    uint64_t pv = in + 4 * ((uint64_t)(r0 - 1) * pitch + cl);                 // vector of row r0 - 1
+    uint64_t ph = in + 4 * ((uint64_t)r0 * pitch + (lane == 0 ? c - 1 : c + 4));   // halo word of row r0
+    uint64_t po = out + 4 * ((uint64_t)r0 * pitch + c);                       // output vector of row r0
+    // counting modes: bit b of refm = the vector of row r0 - 1 + b lies
+    // outside the partition (one predicated OR per load, the bit a
+    // compile-time constant); its refused logical accesses are weighted
+    // after the loop by the points that use it (see below)
+    uint32_t refm = 0;
+    // modulo with WALK (no lane's strip straddles the base and a row step
+    // is below the partition size): each vector's fence follows from the
+    // previous row's (Fence::step_up), an edge lane's halo word from the
+    // fence of the vector of the row below it (step_down) and each output
+    // vector from the previous output row's; every access still gets its own
+    // fenced address, equal to the full modulo.
+    uint64_t fv = 0, fo = 0;
+    auto ldv = [&](int b) {                            // the vector of row r0 - 1 + b, at pv
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if constexpr (MODE == kModulo && WALK) {
-            f_last = r == r0 - 1 ? f16.addr(a) : f16.step_up(f_last, 4 * pitch);
-            return __ldg(reinterpret_cast<const float4 *>(f_last));
-        }
-        const bool ok = counts(MODE) ? (a - f16.base) <= f16.lim : true;    // a is 16-aligned (API)
-        if constexpr (counts(MODE)) nv += ok ? 0u : weight(r);
-        if constexpr (MODE == kClamp) {
-            if (ok) return __ldg(reinterpret_cast<const float4 *>(a));
-            const float w = __ldg(reinterpret_cast<const float *>(f16.edge4(a)));
-            return make_float4(w, w, w, w);
-        } else if constexpr (MODE == kCheck) {
-            // predicated: the destination is zeroed before the load, so
-            // nothing consumes the loaded value until the stencil uses it
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (ok) v = __ldg(reinterpret_cast<const float4 *>(a));
-            return v;
+            fv = b == 0 ? f16.addr(pv) : f16.step_up(fv, step);
+            v = __ldg(reinterpret_cast<const float4 *>(fv));
+        } else if constexpr (counts(MODE)) {
+            const bool ok = (pv - f16.base) <= f16.lim;                       // pv is 16-aligned (API)
+            if (!ok) refm |= 1u << b;
+            if constexpr (MODE == kClamp) {
+                // a clamped outside vector is its edge word four times (fence.cuh
+                // vld4): branch-free, the edge vector (first or last 16 bytes of
+                // the partition) is loaded instead and its edge word splatted
+                const bool below = pv < f16.base;
+                const uint64_t la = ok ? pv : (below ? f16.base : f16.base + f16.lim);
+                v = __ldg(reinterpret_cast<const float4 *>(la));
+                if (!ok) {
+                    const float w = below ? v.x : v.w;
+                    v = make_float4(w, w, w, w);
+                }
+            } else if constexpr (MODE == kCheck) {
+                // predicated: the destination is zeroed before the load
+                if (ok) v = __ldg(reinterpret_cast<const float4 *>(pv));
+            } else {
+                v = __ldg(reinterpret_cast<const float4 *>(f16.addr(pv)));
+            }
         } else {
-            return __ldg(reinterpret_cast<const float4 *>(f16.addr(a)));
+            v = __ldg(reinterpret_cast<const float4 *>(f16.addr(pv)));
+        }
+        return v;
+    };
+    auto ldh = [&]() {                                 // an edge lane's halo word, at ph (pv: the row below)
+        float v = 0.f;
+        if constexpr (MODE == kModulo && WALK) {
+            if (need_h) v = __ldg(reinterpret_cast<const float *>(f4.step_down(fv, pv - ph)));
+        } else if constexpr (counts(MODE)) {
+            const bool ok = (ph - f4.base) <= f4.lim;                         // ph is 4-aligned
+            if (need_h && !ok) nv++;
+            if constexpr (MODE == kCheck) {
+                if (need_h && ok) v = __ldg(reinterpret_cast<const float *>(ph));
+            } else {
+                if (need_h) v = __ldg(reinterpret_cast<const float *>(f4.addr(ph)));
+            }
+        } else {
+            if (need_h) v = __ldg(reinterpret_cast<const float *>(f4.addr(ph)));
+        }
+        return v;
+    };
+    auto stv = [&](int row, const float (&o)[4]) {    // the output vector at po
+        if constexpr (MODE == kModulo && WALK) {
+            fo = row == 0 ? f16.addr(po) : f16.step_up(fo, step);             // F4(po + 4k) = F16(po) + 4k
+            if (all4) {
+                st_v(fo, make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
+                                    __float_as_uint(o[3])));
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    if (interior[k]) *reinterpret_cast<float *>(fo + 4 * k) = o[k];
+            }
+        } else if (all4a) {                            // the common case: one 16-byte store
+            const uint4 val = make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
+                                         __float_as_uint(o[3]));
+            if constexpr (MODE == kClamp) {
+                vst4(f16, po, val, nv, st_v, st_w);     // (po is 16-aligned)
+            } else {
+                if (f16.go_aligned(po, nv, 4)) st_v(f16.addr(po), val);          // po is 16-aligned
+            }
+        } else if (active) {                           // the grid's first / last columns
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                if (!interior[k]) continue;
+                const uint64_t a = po + 4 * k;
+                if (f4.go_aligned(a, nv, 1)) *reinterpret_cast<float *>(f4.addr(a)) = o[k];   // a is 4-aligned
+            }
         }
     };
-    auto lds = [&](uint64_t e, uint64_t a_below) {     // one logical access of one point
-        const uint64_t a = in + 4 * e;
-        if constexpr (MODE == kModulo && WALK) {       // f_last: the fence of the vector of the row below
-            return __ldg(reinterpret_cast<const float *>(f4.step_down(f_last, a_below - a)));
-        }
-        const bool ok = counts(MODE) ? (a - f4.base) <= f4.lim : true;      // a is 4-aligned
-        if constexpr (counts(MODE)) nv += ok ? 0u : 1u;
-        if constexpr (MODE == kCheck) {
-            float v = 0.f;
-            if (ok) v = __ldg(reinterpret_cast<const float *>(a));
-            return v;
-        } else {
-            return __ldg(reinterpret_cast<const float *>(f4.addr(a)));
-        }
-    };
-    float4 P = ldv(r0 - 1);
-    float4 Cv = ldv(r0);
-    for (uint32_t r = r0; r < r1; r += kG) {
+    float4 P = ldv(0);
+    pv += step;
+    float4 Cv = ldv(1);
+    pv += step;
+#pragma unroll
+    for (int i = 0; i < ROWS; i += kG) {
+        if (!FULL && r0 + i >= r1) break;              // uniform over the CTA
         float4 S[kG];
-        float wv[kG], ev[kG];
+        float hv[kG];
 #pragma unroll
         for (int g = 0; g < kG; g++) {
-            const uint32_t rr = r + g;
             S[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-            wv[g] = ev[g] = 0.f;
-            if (rr < r1) {
-                S[g] = ldv(rr + 1);
-                if (interior[0]) wv[g] = lds((uint64_t)rr * pitch + c - 1, in + 4 * ((uint64_t)(rr + 1) * pitch + c));
-                if (interior[3]) ev[g] = lds((uint64_t)rr * pitch + c + 4, in + 4 * ((uint64_t)(rr + 1) * pitch + c));
+            hv[g] = 0.f;
+            if (FULL || r0 + i + g < r1) {
+                S[g] = ldv(i + g + 2);
+                hv[g] = ldh();
+                pv += step;
+                ph += step;
             }
         }
 #pragma unroll
         for (int g = 0; g < kG; g++) {
-            const uint32_t rr = r + g;
-            if (rr < r1) {
+            if (FULL || r0 + i + g < r1) {
                 const float4 N = (g == 0) ? P : ((g == 1) ? Cv : S[g >= 2 ? g - 2 : 0]);
                 const float4 C = (g == 0) ? Cv : S[g >= 1 ? g - 1 : 0];
+                const float wl = __shfl_up_sync(0xffffffffu, C.w, 1);
+                const float er = __shfl_down_sync(0xffffffffu, C.x, 1);
                 const float cn[4] = {N.x, N.y, N.z, N.w};
                 const float cc[4] = {C.x, C.y, C.z, C.w};
                 const float cs[4] = {S[g].x, S[g].y, S[g].z, S[g].w};
                 float o[4];
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
-                    const float w = (k == 0) ? wv[g] : cc[k - 1];
-                    const float e = (k == 3) ? ev[g] : cc[k + 1];
+                    const float w = (k == 0) ? __uint_as_float((__float_as_uint(wl) & ~m0) | (__float_as_uint(hv[g]) & m0))
+                                             : cc[k - 1];
+                    const float e = (k == 3) ? __uint_as_float((__float_as_uint(er) & ~m31) | (__float_as_uint(hv[g]) & m31))
+                                             : cc[k + 1];
                     const float ns = __fadd_rn(cn[k], cs[k]);
                     const float we = __fadd_rn(w, e);
                     const float s = __fadd_rn(ns, we);
                     o[k] = __fmaf_rn(c1, s, __fmul_rn(c0, cc[k]));
                 }
-                const uint64_t ao = out + 4 * ((uint64_t)rr * pitch + c);
-                if constexpr (MODE == kModulo && WALK) {
-                    // F4(ao + 4k) = F16(ao) + 4k
-                    fo_last = rr == r0 ? f16.addr(ao) : f16.step_up(fo_last, 4 * pitch);
-                    if (all4) {
-                        st_v(fo_last, make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
-                                                 __float_as_uint(o[3])));
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 4; k++)
-                            if (interior[k]) *reinterpret_cast<float *>(fo_last + 4 * k) = o[k];
-                    }
-                } else if (all4) {
-                    vst4(f16, ao,
-                         make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
-                                    __float_as_uint(o[3])),
-                         nv, st_v, st_w);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        if (!interior[k]) continue;
-                        const uint64_t a = ao + 4 * k;
-                        if (f4.go(a, nv, 1)) *reinterpret_cast<float *>(f4.addr(a)) = o[k];
-                    }
-                }
+                stv(i + g, o);
+                po += step;
             }
         }
         // slide the window: rows r+kG-1 (new P) and r+kG (new C)
@@ -172,14 +212,38 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         else P = Cv;
         Cv = S[kG - 1];
     }
+    if constexpr (counts(MODE) && !(MODE == kModulo && WALK)) {
+        // the vector of row x = r0 - 1 + b is loaded by the interior points of
+        // row x + 1 as N (bits 0 .. n-1), of row x as C (each), W (k >= 1), E
+        // (k <= 2), and as lane+1's W / lane-1's E within the warp (bits
+        // 1 .. n), of row x - 1 as S (bits 2 .. n+1), n = r1 - r0 rows
+        if (refm) {
+            uint32_t ni = 0, nCv = 0;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                ni += interior[k];
+                nCv += interior[k] * (1u + (k >= 1) + (k <= 2));
+            }
+            nCv += (uint32_t)(lane < 31 && c + 6 <= W) + (uint32_t)(lane > 0 && active);
+            const uint32_t m = (1u << (r1 - r0)) - 1u;
+            nv += ni * (__popc(refm & m) + __popc(refm & (m << 2))) + nCv * __popc(refm & (m << 1));
+        }
+    }
+}
+
+// The strip of a CTA's rows, full (the common case) or the grid's last, shorter one.
+template <int MODE, int kG, int ROWS, bool WALK = false>
+__device__ __forceinline__ void strip_rows(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t W,
+                                           uint64_t pitch, float c0, float c1, uint64_t c, uint32_t r0, uint32_t r1,
+                                           uint32_t &nv) {
+    if (r1 - r0 == ROWS) strip<MODE, kG, ROWS, true, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+    else strip<MODE, kG, ROWS, false, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
 }
 
 // ROWS (rows per CTA strip) is a compile-time constant: 16-row strips at HBM
 // sizes (the 2-row halo re-reads hit L2; measured 8 / 16 / 32 / 64 / 128 rows:
 // 6.5 / 6.8 / 6.5 / 6.4 / 6.36 TB/s), 8 rows when that leaves fewer than 4
-// CTAs per SM (L2-resident sizes); as a constant it also keeps the fenced
-// variants (hoisted body + per-access body) inside 64 registers with no
-// local memory.
+// CTAs per SM (L2-resident sizes); the row loop unrolls over it.
 template <int MODE, int ROWS>
 __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                          uint64_t in, uint32_t H, uint32_t W, uint64_t pitch,
@@ -188,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__
     const uint64_t c = 4ull * ((uint64_t)blockIdx.x * kThreads + threadIdx.x);
     const uint32_t r0 = 1u + blockIdx.y * (uint32_t)ROWS;
     const uint32_t r1 = (r0 + ROWS < H - 1) ? r0 + ROWS : H - 1;
+    if (r0 >= r1) return;                              // uniform over the CTA
     if constexpr (hoistable(MODE)) {
         // conservative extents of everything the CTA's strip touches (from
         // blockIdx only, so the test runs on the uniform datapath); inside the
@@ -199,21 +264,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__
         const uint64_t lo_out = out + 4 * (r0 * pitch + cb), hi_out = out + 4 * ((r1 - 1) * pitch + ce);
         if (lo_in < hi_in && lo_out < hi_out && range_in(fd, lo_in, hi_in - lo_in) &&
             range_in(fd, lo_out, hi_out - lo_out)) {
-            if (c < W && r0 < r1) strip<kNone, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+            strip_rows<kNone, 4, ROWS>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
             return;
         }
-        if (c < W && r0 < r1) strip<MODE, 1>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+        strip<MODE, 1, ROWS, false>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
     } else {
-        if (c < W && r0 < r1) strip<MODE, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+        strip_rows<MODE, 4, ROWS>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
     }
     if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }
 
-// Per-access fencing (fd.flags & kNoHoist, GD_CHECK_PER_ACCESS=1, the
-// paper's instrumentation): no range test, every strip runs the fenced body
-// with 4 rows of loads in flight, inside 64 registers in every mode (the
-// hoisted kernel's edge body keeps one row in flight next to its unfenced
-// body).
+// Per-access fencing (GD_FENCE_PER_ACCESS, fd.flags & kNoHoist, the paper's
+// instrumentation): no range test, every strip runs the fenced body with 4
+// rows of loads in flight.
 template <int MODE, int ROWS>
 __global__ void __launch_bounds__(kThreads, 4) k_stencil_pa(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                             uint64_t in, uint32_t H, uint32_t W, uint64_t pitch,
@@ -222,22 +285,24 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_pa(const __grid_constan
     const uint64_t c = 4ull * ((uint64_t)blockIdx.x * kThreads + threadIdx.x);
     const uint32_t r0 = 1u + blockIdx.y * (uint32_t)ROWS;
     const uint32_t r1 = (r0 + ROWS < H - 1) ? r0 + ROWS : H - 1;
-    if (c < W && r0 < r1) {
-        if constexpr (MODE == kModulo) {
-            // the walk recurrence holds when no operand range of the strip
-            // straddles the base (the u64 offsets do not wrap) and a row step
-            // is below the partition size
-            const uint64_t lo_in = in + 4 * ((r0 - 1) * pitch + c) - (c ? 4 : 0);
-            const uint64_t hi_in = in + 4 * (r1 * pitch + c + 5);
-            const uint64_t lo_out = out + 4 * (r0 * pitch + c), hi_out = out + 4 * ((r1 - 1) * pitch + c + 4);
-            const auto side = [&](uint64_t lo, uint64_t hi) { return lo <= hi && (hi <= fd.base || lo >= fd.base); };
-            if (4 * pitch < fd.size && side(lo_in, hi_in) && side(lo_out, hi_out))
-                strip<MODE, 4, true>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
-            else
-                strip<MODE, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
-        } else {
-            strip<MODE, 4>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
-        }
+    if (r0 >= r1) return;                              // uniform over the CTA
+    if constexpr (MODE == kModulo) {
+        // the walk recurrence holds when no operand range of the strip
+        // straddles the base (the u64 offsets do not wrap) and a row step is
+        // below the partition size; decided for the whole warp (shuffles)
+        // (a lane past the width walks the loads of the row's last vector)
+        const uint64_t cl = c < W ? c : ((uint64_t)(W - 1) & ~3ull);
+        const uint64_t lo_in = in + 4 * ((r0 - 1) * pitch + cl) - (cl ? 4 : 0);
+        const uint64_t hi_in = in + 4 * (r1 * pitch + cl + 5);
+        const uint64_t lo_out = out + 4 * (r0 * pitch + cl), hi_out = out + 4 * ((r1 - 1) * pitch + cl + 4);
+        const auto side = [&](uint64_t lo, uint64_t hi) { return lo <= hi && (hi <= fd.base || lo >= fd.base); };
+        const bool walk = 4 * pitch < fd.size && side(lo_in, hi_in) && side(lo_out, hi_out);
+        if (__all_sync(0xffffffffu, walk))
+            strip_rows<MODE, 4, ROWS, true>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+        else
+            strip<MODE, 4, ROWS, false>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+    } else {
+        strip_rows<MODE, 4, ROWS>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
     }
     if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }

@@ -57,8 +57,20 @@ def _run(a, p, mode, A, B, C, M, N, K, lda, ldb, ldc, exact=False, expect_viol=N
         nr = np.linalg.norm(r)
         rel = np.linalg.norm(g - r) / (nr if nr else 1.0)
         assert rel <= 1e-2, rel
-        print(f"gemm {M}x{N}x{K} {mode}: rel Frobenius {rel:.2e}")
+        # element-wise (DESIGN.md R-GEMM): |g - r| <= 2 ulp_bf16(r) + 2^-16 S, S = sum_k |a_k b_k|
+        # <= K for the U[-1,1) operands here
+        tol = 2 * bf16_ulp(r) + 2.0 ** -16 * K
+        bad = np.abs(g - r) > tol
+        assert not bad.any(), (int(bad.sum()), float(np.abs(g - r).max()))
+        print(f"gemm {M}x{N}x{K} {mode}: rel Frobenius {rel:.2e}, max |err| {np.abs(g - r).max():.2e}")
     return c
+
+
+def bf16_ulp(x):
+    """Spacing of bf16 numbers at |x| (8 significant bits): 2^(e-8) for
+    |x| = m 2^e, 0.5 <= m < 1; the smallest normal spacing at 0."""
+    _, e = np.frexp(np.abs(x))
+    return np.ldexp(1.0, np.maximum(e - 8, -133))
 
 
 @pytest.mark.parametrize("mode", ["none", "mask", "check"])

@@ -118,3 +118,39 @@ def test_check_in_outside_reads_all_zero():
     o = m.view(out, np.float32, H * pitch).reshape(H, pitch)
     assert (o[1:H - 1, 1:W - 1] == 0).all() and (o[0] == 7).all() and (o[:, W - 1] == 7).all()
     assert c.violations == H
+
+
+@pytest.mark.parametrize("mode", ["mask", "check", "clamp", "modulo", "maskcount"])
+@pytest.mark.parametrize("shift", [0, 4, 16, 60, 100, 4 * 39, 4 * 41])
+def test_out_rows_stored_iff_every_interior_point_inside(mode, shift):
+    """Reading R-TMA-out, pinned without the extent formula:
+    K5 v2 stores whole rows.  With `out` crossing the partition end, row r's
+    interior points are stored iff EVERY interior point of row r lies in the
+    partition (byte membership of each 4-byte point, enumerated here), and a
+    row that is only partly inside keeps all its old bytes -- unlike v1's
+    per-access fence, which stores (mask: wraps) each point on its own.  The
+    sweep of `shift` moves the end across every column position of a row."""
+    rng = synth.rng_for(74)
+    H, W, pitch = 14, 41, 44
+    f = synth.uniform_f32(rng, H * pitch, 0.0, 1.0).reshape(H, pitch)
+    m = oracle.Mem(PBASE, PSIZE)
+    m.write(PBASE, f.reshape(-1))
+    out = PBASE + PSIZE - 6 * 4 * pitch - shift            # rows 6.. cross or pass the end
+    out -= out % 16
+    sentinel = np.full(((PBASE + PSIZE) - out) // 4, 0x7F7F7F7F, np.uint32)
+    m.write(out, sentinel)
+    oracle.stencil_tma(m, PBASE, PSIZE, mode, out, PBASE, H, W, pitch, float(C0), float(C1))
+    ref = _ref(f, H, W)
+    end = PBASE + PSIZE
+    for r in range(1, H - 1):
+        pts = [out + 4 * (r * pitch + col) for col in range(1, W - 1)]
+        inside = [all(PBASE <= b < end for b in range(x, x + 4)) for x in pts]
+        whole = all(inside)
+        for col, x, ins in zip(range(1, W - 1), pts, inside):
+            if not ins:
+                continue                                   # not in this partition's memory
+            got = m.view(x, np.uint32, 1)[0]
+            if whole:
+                assert got == ref[r - 1, col - 1].view(np.uint32), (r, col)
+            else:
+                assert got == 0x7F7F7F7F, (r, col)          # partly inside: the row is not stored
