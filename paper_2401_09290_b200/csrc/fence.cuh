@@ -112,6 +112,8 @@ struct Fence {
             return true;
         }
     }
+    // inside(a) for an address the caller has proven W-aligned
+    __device__ __forceinline__ bool ok_aligned_in(uint64_t a) const { return (a - base) <= lim; }
     // CLAMP, for a 16-byte vector of four logical 4-byte elements wholly
     // outside the partition: the word every one of its elements clamps to
     __device__ __forceinline__ uint64_t edge4(uint64_t a) const { return a < base ? base : base + size - 4; }
@@ -124,16 +126,19 @@ struct Fence {
 // CLAMP sends all four elements of an outside vector to one edge word, so the
 // vector is that word four times (a store keeps the last element, element
 // order).  Counted 4 per vector.  LD16 / LD4 / ST16 / ST4 are the cache
-// operators of the call site.
+// operators of the call site.  Precondition: a is 16-byte aligned (every
+// call site indexes a 16-byte-aligned buffer in 16-byte steps; the API
+// refuses misaligned buffers), so the alignment half of the check predicate
+// is known true.
 template <int MODE, typename LD16, typename LD4>
 __device__ __forceinline__ uint4 vld4(const Fence<MODE, 16> &f, uint64_t a, uint32_t &nv, LD16 ld16, LD4 ld4) {
     if constexpr (MODE == kClamp) {
-        if (f.inside(a)) return ld16(a);
+        if (f.ok_aligned_in(a)) return ld16(a);
         nv += 4;
         const uint32_t w = ld4(f.edge4(a));
         return make_uint4(w, w, w, w);
     } else {
-        if (f.go(a, nv, 4)) return ld16(f.addr(a));
+        if (f.go_aligned(a, nv, 4)) return ld16(f.addr(a));
         return make_uint4(0, 0, 0, 0);
     }
 }
@@ -142,14 +147,14 @@ template <int MODE, typename ST16, typename ST4>
 __device__ __forceinline__ void vst4(const Fence<MODE, 16> &f, uint64_t a, uint4 v, uint32_t &nv, ST16 st16,
                                      ST4 st4) {
     if constexpr (MODE == kClamp) {
-        if (f.inside(a)) {
+        if (f.ok_aligned_in(a)) {
             st16(a, v);
         } else {
             nv += 4;
             st4(f.edge4(a), v.w);
         }
     } else {
-        if (f.go(a, nv, 4)) st16(f.addr(a), v);
+        if (f.go_aligned(a, nv, 4)) st16(f.addr(a), v);
     }
 }
 
@@ -164,25 +169,16 @@ __device__ __forceinline__ bool range_in(const FenceDesc &fd, uint64_t a, uint64
     return !(fd.flags & kNoHoist) && len <= fd.size && off <= fd.size - len;
 }
 
-// Sum a per-thread refusal count over the CTA and add it to the trusted
-// counter with one atomic per CTA.  All threads of the
-// CTA must call it.
+// Add the refusal counts of a warp to the trusted counter: nothing when no
+// lane counted (the common case, one vote), else a warp reduction and one
+// 64-bit atomic from lane 0 (warp-level aggregation of
+// the violation counters).  No CTA-wide barrier, so warps that finish early
+// are not held back.  Every lane of a full warp must call it (the per-thread
+// counts are small: their warp sum fits 32 bits).
 __device__ __forceinline__ void flush_violations(uint32_t nv_thread, unsigned long long *viol) {
-    if (!__syncthreads_or(nv_thread != 0)) return;    // common case: nothing refused in this CTA
-    __shared__ unsigned long long warp_sums[32];
-    uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    unsigned long long nv = nv_thread;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
-    if (lane == 0) warp_sums[warp] = nv;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t nw = (blockDim.x + 31u) >> 5;
-        unsigned long long s = lane < nw ? warp_sums[lane] : 0ull;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0 && s) atomicAdd(viol, s);
-    }
+    if (!__any_sync(0xffffffffu, nv_thread != 0)) return;
+    const uint32_t s = __reduce_add_sync(0xffffffffu, nv_thread);
+    if ((threadIdx.x & 31u) == 0) atomicAdd(viol, (unsigned long long)s);
 }
 
 }  // namespace gd

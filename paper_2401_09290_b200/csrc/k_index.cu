@@ -81,7 +81,7 @@ __device__ __forceinline__ void gather_chunk(const FenceDesc &fd, uint64_t out, 
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_gather1(const __grid_constant__ FenceDesc fd, uint64_t out,
+__global__ void __launch_bounds__(kThreads, 5) k_gather1(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                       uint64_t table, uint64_t idx, uint64_t nvec, uint32_t tail) {
     uint32_t nv = 0;
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, v0 = c0 + threadIdx.x;
@@ -326,7 +326,7 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
 // 5 CTAs measured 27-41 % slower at D = 32 / 64; clamp with G = 4 needs the
 // registers of 5 (no spill) and loses nothing there (D = 128).
 template <int MODE, int G, bool P2>
-__global__ void __launch_bounds__(kThreads, (MODE == kClamp && G == 4) ? 5 : 6) k_gatherR(const __grid_constant__ FenceDesc fd, uint64_t out,
+__global__ void __launch_bounds__(kThreads, (MODE == kClamp && G >= 2) ? 5 : 6) k_gatherR(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                       uint64_t table, uint64_t idx, uint64_t nslots, uint32_t tpr,
                                                       uint64_t dv) {
     constexpr uint64_t ch = (uint64_t)kThreads * (4 / G);
@@ -501,6 +501,16 @@ cudaError_t gather_t(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t
 
 template <int MODE>
 cudaError_t scatter_t(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src, uint64_t n, cudaStream_t s) {
+    // large scatters: radix-partitioned by partition slice (k_scatter.cu);
+    // the direct kernel takes the rest, or the n % 4 tail
+    const cudaError_t b = launch_scatter_bucketed(MODE, fd, table, idx, src, n, s);
+    if (b == cudaSuccess) {
+        if (n % 4 == 0) return cudaSuccess;
+        const uint64_t done = n / 4 * 16;
+        k_scatter<MODE><<<1, kThreads, 0, s>>>(fd, table, idx + done, src + done, 0, (uint32_t)(n % 4));
+        return cudaGetLastError();
+    }
+    if (b != cudaErrorNotSupported) return b;
     k_scatter<MODE><<<chunk_grid(n / 4), kThreads, 0, s>>>(fd, table, idx, src, n / 4, (uint32_t)(n % 4));
     return cudaGetLastError();
 }

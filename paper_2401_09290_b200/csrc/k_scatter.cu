@@ -1,0 +1,310 @@
+// k_scatter.cu -- K4 v2: the fenced embedding-style scatter-add,
+// table[sext(idx[i])] += src[i] (u32), radix-partitioned by partition slice
+// for sm_100a (the per-access fence of PAPER.md:230).
+//
+// Why: a random 4-byte read-modify-write into a table far larger than L2
+// costs two random DRAM transactions (the sector fill and, later, its dirty
+// write-back).  tools/scatter_probe.cu measures 22.6 G random REDs/s into a
+// 2 GiB table against 50.4 G random reads/s and 195 G REDs/s into an
+// L2-resident (<= 64 MiB) table: the direct kernel (k_index.cu k_scatter) is
+// bound by the DRAM's random-transaction rate, not by bytes.  Applying the
+// updates one partition slice at a time keeps each slice's table lines in L2
+// while they are updated, so the fills and write-backs of a slice happen
+// close together in time and address.
+//
+//   A1  k_scatter_part<M, 0>  every index: its fenced address -> slice id;
+//                             per-CTA shared histogram, one global atomic
+//                             per non-empty slice
+//   A2  k_scatter_scan        exclusive scan of the slice counts (one CTA)
+//   A3  k_scatter_part<M, 1>  the same fence again, refusals counted (once,
+//                             here), each update placed as (word offset,
+//                             value) in its slice's run of the scratch
+//   B   k_scatter_apply       the runs in slice order: RED.ADD.U32 at
+//                             base + 4 * word (CTAs in flight cover about one
+//                             slice, so its lines stay in L2)
+//
+// Every logical access is fenced exactly as in the direct kernel and as the
+// oracle defines it (or_scatter_add): the index and source loads per access
+// or per CTA tile (R-hoist), the read-modify-write at its own fenced address
+// (one logical access), each refusal counted once.  u32 addition
+// is commutative and associative, so the order of the updates does not
+// change the result (reading A6).  Clamped RMWs of a CTA are summed per edge
+// word and added by one atomic each (as in k_scatter).  In NONE mode an
+// address outside the partition is updated directly, unfenced (the native
+// twin).  The scratch (8 bytes per update) is trusted memory outside every
+// partition, allocated stream-ordered (cudaMallocAsync) per launch, so
+// concurrent tenants never share it; a placement past its slice's run (only
+// possible if the tenant rewrites idx while its own launch runs) is dropped,
+// never written outside the scratch.
+#include "fence.cuh"
+#include "kernels.h"
+
+namespace gd {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kU = 4;                                  // 16-byte index vectors per thread
+constexpr uint64_t kChunk = (uint64_t)kThreads * kU;   // vectors (4 indices each) per CTA
+constexpr int kSliceShift = 25;                        // 32 MiB slices
+constexpr uint32_t kMaxSlices = 512;                   // partitions up to 16 GiB (u32 word offsets)
+
+__device__ __forceinline__ uint4 ld_u4(uint64_t a) { return __ldcs(reinterpret_cast<const uint4 *>(a)); }
+__device__ __forceinline__ uint32_t ld_w(uint64_t a) { return __ldcs(reinterpret_cast<const unsigned int *>(a)); }
+
+struct EdgeAcc {                                       // clamped RMWs of a thread, per edge word
+    uint32_t lo = 0, hi = 0;
+    bool alo = false, ahi = false;
+};
+
+__device__ __forceinline__ void edge_add(const FenceDesc &fd, const EdgeAcc &es) {
+    __shared__ uint32_t sum[2], any[2];
+    if (threadIdx.x < 2) sum[threadIdx.x] = any[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t lo = __reduce_add_sync(0xffffffffu, es.lo), hi = __reduce_add_sync(0xffffffffu, es.hi);
+    const bool alo = __any_sync(0xffffffffu, es.alo), ahi = __any_sync(0xffffffffu, es.ahi);
+    if ((threadIdx.x & 31u) == 0) {
+        if (alo) { atomicAdd(&sum[0], lo); any[0] = 1; }
+        if (ahi) { atomicAdd(&sum[1], hi); any[1] = 1; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && any[0]) atomicAdd(reinterpret_cast<unsigned int *>(fd.base), sum[0]);
+    if (threadIdx.x == 1 && any[1]) atomicAdd(reinterpret_cast<unsigned int *>(fd.base + fd.size - 4), sum[1]);
+}
+
+// One RMW of the direct kernel's semantics, resolved: *word = partition word
+// offset of the fenced address when it is to be bucketed (returns true);
+// otherwise counted / clamped / (NONE, outside) applied directly in pass 1.
+template <int MODE, int PASS>
+__device__ __forceinline__ bool resolve(const Fence<MODE, 4> &f4, uint64_t table, int32_t j, uint32_t v,
+                                        uint32_t &nv, EdgeAcc &es, uint64_t &word) {
+    const uint64_t a = table + (uint64_t)((int64_t)j * 4);        // sext, scale in 64 bits (Listing 1 l.22)
+    if constexpr (MODE == kNone) {
+        if (a - f4.base <= f4.lim && (a & 3) == 0) {
+            word = (a - f4.base) >> 2;
+            return true;
+        }
+        if (PASS == 1) atomicAdd(reinterpret_cast<unsigned int *>(a), v);   // the native twin: unfenced
+        return false;
+    } else if constexpr (MODE == kClamp) {
+        if (f4.inside(a)) {
+            word = (a - f4.base) >> 2;
+            return true;
+        }
+        if (PASS == 1) {
+            nv++;
+            if (a < f4.base) {
+                es.lo += v;
+                es.alo = true;
+            } else {
+                es.hi += v;
+                es.ahi = true;
+            }
+        }
+        return false;
+    } else {
+        uint32_t c = 0;
+        const bool ok = f4.go(a, c, 1);                               // check: refused; mask-count: counted
+        if (PASS == 1) nv += c;
+        if (!ok) return false;
+        word = (f4.addr(a) - f4.base) >> 2;
+        return true;
+    }
+}
+
+// The 16 updates of one thread (A1 / A3): loads, fence, slice rank.
+// SMODE fences the idx / src streams (kNone when the CTA's tiles of both lie
+// in the partition: R-hoist), MODE the RMWs.  Bit k of *putm: update k is
+// bucketed at partition word w[k], rank rk[k] in its slice's CTA histogram.
+constexpr int kItems = 4 * kU;
+
+template <int SMODE, int MODE, int PASS>
+__device__ __forceinline__ void items(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src, uint64_t v0,
+                                      uint64_t nvec, uint32_t &nv, EdgeAcc &es, unsigned *hist,
+                                      uint32_t (&w)[kItems], uint32_t (&rk)[kItems], uint32_t (&sv)[kItems],
+                                      uint32_t &putm) {
+    const Fence<SMODE, 16> f16(fd);
+    const Fence<MODE, 4> f4(fd);
+    uint4 j[kU], s[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+        const uint64_t v = v0 + u * kThreads;
+        j[u] = make_uint4(0, 0, 0, 0);
+        s[u] = make_uint4(0, 0, 0, 0);
+        if (v < nvec) {
+            uint32_t c = 0;
+            j[u] = vld4(f16, idx + 16 * v, c, ld_u4, ld_w);
+            if (PASS == 1) s[u] = vld4(f16, src + 16 * v, c, ld_u4, ld_w);
+            if (PASS == 1) nv += c;
+        }
+    }
+    putm = 0;
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+        const bool live = v0 + u * kThreads < nvec;
+        const uint32_t jj[4] = {j[u].x, j[u].y, j[u].z, j[u].w}, ss[4] = {s[u].x, s[u].y, s[u].z, s[u].w};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int k = 4 * u + q;
+            uint64_t word = 0;
+            const bool put = live && resolve<MODE, PASS>(f4, table, (int32_t)jj[q], ss[q], nv, es, word);
+            w[k] = (uint32_t)word;
+            sv[k] = ss[q];
+            rk[k] = put ? atomicAdd(&hist[w[k] >> (kSliceShift - 2)], 1u) : 0u;
+            putm |= (uint32_t)put << k;
+        }
+    }
+}
+
+template <int MODE, int PASS>
+__global__ void __launch_bounds__(kThreads) k_scatter_part(const __grid_constant__ FenceDesc fd, uint64_t table,
+                                                           uint64_t idx, uint64_t src, uint64_t nvec,
+                                                           uint32_t nslices, unsigned *cnt, unsigned *cur,
+                                                           const unsigned *lim, uint2 *pairs) {
+    __shared__ unsigned hist[kMaxSlices];
+    __shared__ unsigned gpos[kMaxSlices];
+    for (uint32_t i = threadIdx.x; i < nslices; i += kThreads) hist[i] = 0;
+    __syncthreads();
+    uint32_t nv = 0, putm = 0;
+    uint32_t w[kItems], rk[kItems], sv[kItems];
+    EdgeAcc es;
+    const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, v0 = c0 + threadIdx.x;
+    if constexpr (hoistable(MODE)) {                   // streams hoisted per CTA tile; RMWs fenced one by one
+        const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
+        if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, src + 16 * c0, 16 * cn))
+            items<kNone, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
+        else
+            items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
+    } else {
+        items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
+    }
+    __syncthreads();
+    if constexpr (PASS == 0) {
+        for (uint32_t i = threadIdx.x; i < nslices; i += kThreads)
+            if (hist[i]) atomicAdd(&cnt[i], hist[i]);
+    } else {
+        // reserve this CTA's run in every slice it updates, then place
+        for (uint32_t i = threadIdx.x; i < nslices; i += kThreads) gpos[i] = hist[i] ? atomicAdd(&cur[i], hist[i]) : 0u;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kItems; k++) {
+            if (!((putm >> k) & 1u)) continue;
+            const uint32_t b = w[k] >> (kSliceShift - 2);
+            const uint32_t pos = gpos[b] + rk[k];
+            if (pos < lim[b]) pairs[pos] = make_uint2(w[k], sv[k]);
+        }
+        if constexpr (MODE == kClamp) edge_add(fd, es);
+        if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
+    }
+}
+
+// A2: exclusive scan of the slice counts -> run starts (cur) and ends (lim);
+// total = updates placed.  One CTA of kMaxSlices threads.
+__global__ void __launch_bounds__(kMaxSlices) k_scatter_scan(const unsigned *cnt, unsigned *cur, unsigned *lim,
+                                                             unsigned *total, uint32_t nslices) {
+    __shared__ unsigned sh[kMaxSlices];
+    const uint32_t t = threadIdx.x;
+    const unsigned c = t < nslices ? cnt[t] : 0u;
+    sh[t] = c;
+    __syncthreads();
+    for (uint32_t o = 1; o < kMaxSlices; o <<= 1) {  // inclusive Hillis-Steele scan
+        const unsigned add = t >= o ? sh[t - o] : 0u;
+        __syncthreads();
+        sh[t] += add;
+        __syncthreads();
+    }
+    if (t < nslices) {
+        cur[t] = sh[t] - c;
+        lim[t] = sh[t];
+    }
+    if (t == kMaxSlices - 1) *total = sh[t];
+}
+
+// B: the placed updates in slice order.  word < words by construction (the
+// word offset of a fenced address of the partition); tested anyway, so
+// every address this kernel computes provably lies in the partition.
+__global__ void __launch_bounds__(kThreads) k_scatter_apply(uint64_t base, uint64_t words, const uint2 *pairs,
+                                                            const unsigned *total) {
+    const uint64_t n = *total;
+    const uint64_t i0 = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) * 4;
+    if (i0 >= n) return;
+    uint2 p[4];
+    if (i0 + 4 <= n) {
+        const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(pairs + i0));
+        const uint4 b = __ldcs(reinterpret_cast<const uint4 *>(pairs + i0 + 2));
+        p[0] = make_uint2(a.x, a.y);
+        p[1] = make_uint2(a.z, a.w);
+        p[2] = make_uint2(b.x, b.y);
+        p[3] = make_uint2(b.z, b.w);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; q++) p[q] = i0 + q < n ? pairs[i0 + q] : make_uint2(0xFFFFFFFFu, 0u);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+        if (i0 + q < n && p[q].x < words) atomicAdd(reinterpret_cast<unsigned int *>(base + 4ull * p[q].x), p[q].y);
+}
+
+bool pool_ready() {
+    // keep freed scratch in the device's default memory pool (stream-ordered
+    // reuse, no release to the OS at every synchronisation)
+    static const bool ok = [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return false;
+        uint64_t thr = ~0ull;
+        return cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) == cudaSuccess;
+    }();
+    return ok;
+}
+
+template <int MODE>
+cudaError_t bucketed_t(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src, uint64_t n, cudaStream_t s) {
+    const uint64_t nvec = n / 4;
+    const uint32_t nslices = (uint32_t)((fd.size + (1ull << kSliceShift) - 1) >> kSliceShift);
+    const uint64_t meta = 4ull * (3 * kMaxSlices + 4);                 // cnt | cur | lim | total
+    char *scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&scratch), meta + 8 * (4 * nvec) + 16, s);
+    if (e != cudaSuccess) return e;
+    unsigned *cnt = reinterpret_cast<unsigned *>(scratch), *cur = cnt + kMaxSlices, *lim = cur + kMaxSlices;
+    unsigned *total = lim + kMaxSlices;
+    uint2 *pairs = reinterpret_cast<uint2 *>(scratch + meta);
+    const unsigned grid = (unsigned)((nvec + kChunk - 1) / kChunk);
+    e = cudaMemsetAsync(cnt, 0, 4ull * kMaxSlices, s);
+    if (e == cudaSuccess) {
+        k_scatter_part<MODE, 0><<<grid, kThreads, 0, s>>>(fd, table, idx, src, nvec, nslices, cnt, cur, lim, pairs);
+        k_scatter_scan<<<1, kMaxSlices, 0, s>>>(cnt, cur, lim, total, nslices);
+        k_scatter_part<MODE, 1><<<grid, kThreads, 0, s>>>(fd, table, idx, src, nvec, nslices, cnt, cur, lim, pairs);
+        const unsigned gb = (unsigned)((4 * nvec + 4 * kThreads - 1) / (4 * kThreads));
+        k_scatter_apply<<<gb, kThreads, 0, s>>>(fd.base, fd.size / 4, pairs, total);
+        e = cudaGetLastError();
+    }
+    const cudaError_t f = cudaFreeAsync(scratch, s);
+    return e != cudaSuccess ? e : f;
+}
+
+}  // namespace
+
+// The bucketed path for the update vectors (n / 4 * 4 of them; the caller
+// issues the tail of n % 4 with the direct kernel).  cudaErrorNotSupported:
+// not applicable (a partition above 16 GiB, or too few updates to gain),
+// nothing issued.
+cudaError_t launch_scatter_bucketed(int mode, const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src,
+                                    uint64_t n, cudaStream_t s) {
+    static const bool off = [] {
+        const char *e = getenv("GD_SCATTER_DIRECT");
+        return e && e[0] == '1';
+    }();
+    if (off || n < (1ull << 20) || fd.size > (uint64_t)kMaxSlices << kSliceShift || fd.size < (4ull << kSliceShift) ||
+        !pool_ready())
+        return cudaErrorNotSupported;
+    switch (mode) {
+        case kNone: return bucketed_t<kNone>(fd, table, idx, src, n, s);
+        case kMask: return bucketed_t<kMask>(fd, table, idx, src, n, s);
+        case kModulo: return bucketed_t<kModulo>(fd, table, idx, src, n, s);
+        case kMaskCount: return bucketed_t<kMaskCount>(fd, table, idx, src, n, s);
+        case kClamp: return bucketed_t<kClamp>(fd, table, idx, src, n, s);
+        default: return bucketed_t<kCheck>(fd, table, idx, src, n, s);
+    }
+}
+
+}  // namespace gd

@@ -32,9 +32,11 @@ __device__ __forceinline__ void st_v(uint64_t a, uint4 v) { __stcs(reinterpret_c
 __device__ __forceinline__ void st_w(uint64_t a, uint32_t v) { __stcs(reinterpret_cast<unsigned int *>(a), v); }
 
 // One thread's strip: rows [r0, r1) of the 4-column vector at column c
-// (r1 - r0 <= ROWS; FULL: == ROWS), kG rows of loads in flight.  The row
-// loop is unrolled at compile time, addresses advance by one row pitch per
-// row, and every access is fenced at its own address.
+// (r1 - r0 <= ROWS), kG rows of loads in flight.  FULL: r1 - r0 == ROWS and
+// every lane of the warp holds four interior points (the common case: no
+// row guards, one 16-byte store per row).  The row loop is unrolled at
+// compile time, addresses advance by one row pitch per row, and every
+// access is fenced at its own address.
 template <int MODE, int kG, int ROWS, bool FULL, bool WALK = false>
 __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t W, uint64_t pitch,
                                       float c0, float c1, uint64_t c, uint32_t r0, uint32_t r1, uint32_t &nv) {
@@ -44,7 +46,7 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
     const Fence<MODE, 16> f16(fd);
     const Fence<MODE, 4> f4(fd);
     const uint32_t lane = threadIdx.x & 31u;
-    const bool active = c < W;
+    const bool active = FULL || c < W;
     bool interior[4];
     bool all4 = true;
 #pragma unroll
@@ -52,7 +54,7 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         interior[k] = (c + k >= 1) && (c + k + 2 <= W);
         all4 = all4 && interior[k];
     }
-    const bool all4a = all4;                           // (all four interior implies c < W)
+    const bool all4a = FULL || all4;                   // (all four interior implies c < W)
     // The W word of point k = 0 (column c-1) is word 3 of lane-1's vector of
     // the same row, the E word of point k = 3 (column c+4) word 0 of
     // lane+1's: F4(a-4) = F16(a-16)+12 and F4(a+16) = F16(a+16) in every
@@ -94,19 +96,9 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         } else if constexpr (counts(MODE)) {
             const bool ok = (pv - f16.base) <= f16.lim;                       // pv is 16-aligned (API)
             if (!ok) refm |= 1u << b;
-            if constexpr (MODE == kClamp) {
-                // a clamped outside vector is its edge word four times (fence.cuh
-                // vld4): branch-free, the edge vector (first or last 16 bytes of
-                // the partition) is loaded instead and its edge word splatted
-                const bool below = pv < f16.base;
-                const uint64_t la = ok ? pv : (below ? f16.base : f16.base + f16.lim);
-                v = __ldg(reinterpret_cast<const float4 *>(la));
-                if (!ok) {
-                    const float w = below ? v.x : v.w;
-                    v = make_float4(w, w, w, w);
-                }
-            } else if constexpr (MODE == kCheck) {
-                // predicated: the destination is zeroed before the load
+            if constexpr (MODE == kCheck || MODE == kClamp) {
+                // predicated: the destination is zeroed before the load (clamp:
+                // an outside vector is fixed up after its batch of loads, clampfix)
                 if (ok) v = __ldg(reinterpret_cast<const float4 *>(pv));
             } else {
                 v = __ldg(reinterpret_cast<const float4 *>(f16.addr(pv)));
@@ -116,22 +108,32 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         }
         return v;
     };
-    auto ldh = [&]() {                                 // an edge lane's halo word, at ph (pv: the row below)
+    uint32_t hrefm = 0;                                // clamp: bit x of a halo word of row r0 + x outside
+    auto ldh = [&](int hb) {                           // an edge lane's halo word of row r0 + hb, at ph (pv: the row below)
         float v = 0.f;
         if constexpr (MODE == kModulo && WALK) {
             if (need_h) v = __ldg(reinterpret_cast<const float *>(f4.step_down(fv, pv - ph)));
         } else if constexpr (counts(MODE)) {
-            const bool ok = (ph - f4.base) <= f4.lim;                         // ph is 4-aligned
+            const uint64_t fh = f4.addr(ph);
+            const bool ok = MODE == kMaskCount ? fh == ph : (ph - f4.base) <= f4.lim;     // ph is 4-aligned
             if (need_h && !ok) nv++;
-            if constexpr (MODE == kCheck) {
+            if constexpr (MODE == kClamp) {
+                if (need_h && !ok) hrefm |= 1u << hb;
+            }
+            if constexpr (MODE == kCheck || MODE == kClamp) {
                 if (need_h && ok) v = __ldg(reinterpret_cast<const float *>(ph));
             } else {
-                if (need_h) v = __ldg(reinterpret_cast<const float *>(f4.addr(ph)));
+                if (need_h) v = __ldg(reinterpret_cast<const float *>(fh));
             }
         } else {
             if (need_h) v = __ldg(reinterpret_cast<const float *>(f4.addr(ph)));
         }
         return v;
+    };
+    // clamp: an outside vector at a is its edge word four times (fence.cuh vld4)
+    auto clampfix = [&](uint64_t a) {
+        const float w = __ldg(reinterpret_cast<const float *>(f16.edge4(a)));
+        return make_float4(w, w, w, w);
     };
     auto stv = [&](int row, const float (&o)[4]) {    // the output vector at po
         if constexpr (MODE == kModulo && WALK) {
@@ -147,8 +149,17 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         } else if (all4a) {                            // the common case: one 16-byte store
             const uint4 val = make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
                                          __float_as_uint(o[3]));
-            if constexpr (MODE == kClamp) {
-                vst4(f16, po, val, nv, st_v, st_w);     // (po is 16-aligned)
+            if constexpr (MODE == kMaskCount) {
+                const uint64_t f = f16.addr(po);
+                nv += f != po ? 4u : 0u;                // inside iff the fence is the identity
+                st_v(f, val);
+            } else if constexpr (MODE == kClamp) {     // (fence.cuh vst4, po 16-aligned)
+                if ((po - f16.base) <= f16.lim) {
+                    st_v(po, val);
+                } else {                               // rare: the last element wins the edge word
+                    nv += 4;
+                    st_w(f16.edge4(po), val.w);
+                }
             } else {
                 if (f16.go_aligned(po, nv, 4)) st_v(f16.addr(po), val);          // po is 16-aligned
             }
@@ -165,6 +176,10 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
     pv += step;
     float4 Cv = ldv(1);
     pv += step;
+    if constexpr (MODE == kClamp) {
+        if (refm & 1u) P = clampfix(pv - 2 * step);
+        if (refm & 2u) Cv = clampfix(pv - step);
+    }
 #pragma unroll
     for (int i = 0; i < ROWS; i += kG) {
         if (!FULL && r0 + i >= r1) break;              // uniform over the CTA
@@ -176,9 +191,23 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
             hv[g] = 0.f;
             if (FULL || r0 + i + g < r1) {
                 S[g] = ldv(i + g + 2);
-                hv[g] = ldh();
+                hv[g] = ldh(i + g);
                 pv += step;
                 ph += step;
+            }
+        }
+        if constexpr (MODE == kClamp) {                // rare: outside accesses of this batch, after its loads
+            const uint32_t rows = (1u << kG) - 1u;
+            if (((refm >> (i + 2)) & rows) | ((hrefm >> i) & rows)) {
+#pragma unroll
+                for (int g = 0; g < kG; g++) {
+                    if (!(FULL || r0 + i + g < r1)) continue;
+                    if (refm & (1u << (i + g + 2))) S[g] = clampfix(pv - (uint64_t)(kG - g) * step);
+                    if (hrefm & (1u << (i + g))) {
+                        const uint64_t a = ph - (uint64_t)(kG - g) * step;
+                        hv[g] = __ldg(reinterpret_cast<const float *>(f4.addr(a)));
+                    }
+                }
             }
         }
 #pragma unroll
@@ -231,13 +260,16 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
     }
 }
 
-// The strip of a CTA's rows, full (the common case) or the grid's last, shorter one.
+// The strip of a warp's rows: full (ROWS rows, every lane interior: the common
+// case) or not (the grid's last rows, its first / last columns).
 template <int MODE, int kG, int ROWS, bool WALK = false>
 __device__ __forceinline__ void strip_rows(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t W,
                                            uint64_t pitch, float c0, float c1, uint64_t c, uint32_t r0, uint32_t r1,
                                            uint32_t &nv) {
-    if (r1 - r0 == ROWS) strip<MODE, kG, ROWS, true, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
-    else strip<MODE, kG, ROWS, false, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+    if (r1 - r0 == ROWS && __all_sync(0xffffffffu, c >= 1 && c + 5 <= W))   // every lane: 4 interior points
+        strip<MODE, kG, ROWS, true, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+    else
+        strip<MODE, kG, ROWS, false, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
 }
 
 // ROWS (rows per CTA strip) is a compile-time constant: 16-row strips at HBM

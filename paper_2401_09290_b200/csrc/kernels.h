@@ -24,6 +24,11 @@ cudaError_t launch_gather(int mode, const FenceDesc &fd, uint64_t out, uint64_t 
                           uint64_t n, uint32_t D, cudaStream_t s, const Geom &g);
 cudaError_t launch_scatter(int mode, const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src,
                            uint64_t n, cudaStream_t s, const Geom &g);
+// K4 v2 (k_scatter.cu): the scatter-add of the n / 4 * 4 leading updates,
+// radix-partitioned by partition slice; cudaErrorNotSupported (nothing
+// issued) when it does not apply.
+cudaError_t launch_scatter_bucketed(int mode, const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src,
+                                    uint64_t n, cudaStream_t s);
 cudaError_t launch_stencil(int mode, const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t H, uint32_t W,
                            uint64_t pitch, float c0, float c1, cudaStream_t s, const Geom &g);
 cudaError_t launch_fill(uint64_t base, uint64_t offset, uint64_t nbytes, uint32_t pattern, cudaStream_t s,

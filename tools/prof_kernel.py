@@ -25,7 +25,11 @@ def main():
     ap.add_argument("--mode", default="mask")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--D", type=int, default=32, help="row width (words) for --kind gatherrows")
+    ap.add_argument("--pa", action="store_true", help="per-access fencing (GD_FENCE_PER_ACCESS)")
+    ap.add_argument("--l2", action="store_true", help="stencil at the L2-resident size 2048^2")
     a = ap.parse_args()
+    if a.pa:
+        a.mode += "+pa"
     ar = g.Arena(0, 1 << 34)
     p = ar.partition_alloc(1 << 34)
     gen = torch.Generator(device="cuda:0")
@@ -57,7 +61,8 @@ def main():
         elif a.kind == "stencil_tma":
             ar.stencil_tma(p.id, a.mode, b + 8 * GiB, b + 4 * GiB, 32768, 32768, 32768, 0.5, 0.125)
         elif a.kind == "stencil":
-            ar.stencil(p.id, a.mode, b + 8 * GiB, b + 4 * GiB, 32768, 32768, 32768, 0.5, 0.125)
+            hw = 2048 if a.l2 else 32768
+            ar.stencil(p.id, a.mode, b + 8 * GiB, b + 4 * GiB, hw, hw, hw, 0.5, 0.125)
         elif a.kind == "gemm":
             n = 8192
             ar.gemm(p.id, a.mode, b + 2 * n * n * 2, b, b + n * n * 2, n, n, n, n, n, n)
