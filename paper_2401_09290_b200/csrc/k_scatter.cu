@@ -182,15 +182,42 @@ __global__ void __launch_bounds__(kThreads) k_scatter_part(const __grid_constant
         for (uint32_t i = threadIdx.x; i < nslices; i += kThreads)
             if (hist[i]) atomicAdd(&cnt[i], hist[i]);
     } else {
-        // reserve this CTA's run in every slice it updates, then place
-        for (uint32_t i = threadIdx.x; i < nslices; i += kThreads) gpos[i] = hist[i] ? atomicAdd(&cur[i], hist[i]) : 0u;
+        // Reserve this CTA's run in every slice it updates, sort its updates
+        // by slice in shared memory (exclusive scan of the histogram), then
+        // write each run out with consecutive threads on consecutive pairs.
+        __shared__ unsigned lstart[kMaxSlices];
+        __shared__ unsigned wsum[kThreads / 32];
+        __shared__ uint2 staged[kThreads * kItems];
+        const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+        const uint32_t a0 = 2 * t < nslices ? hist[2 * t] : 0u, a1 = 2 * t + 1 < nslices ? hist[2 * t + 1] : 0u;
+        uint32_t run = a0 + a1;                        // inclusive scan, two slices per thread
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, run, o);
+            if (lane >= (uint32_t)o) run += y;
+        }
+        if (lane == 31) wsum[warp] = run;
+        for (uint32_t i = t; i < nslices; i += kThreads) gpos[i] = hist[i] ? atomicAdd(&cur[i], hist[i]) : 0u;
+        __syncthreads();
+        uint32_t pre = 0, total = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < kThreads / 32; k++) {
+            pre += k < warp ? wsum[k] : 0u;
+            total += wsum[k];
+        }
+        const uint32_t ex = pre + run - (a0 + a1);
+        if (2 * t < nslices) lstart[2 * t] = ex;
+        if (2 * t + 1 < nslices) lstart[2 * t + 1] = ex + a0;
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kItems; k++) {
-            if (!((putm >> k) & 1u)) continue;
-            const uint32_t b = w[k] >> (kSliceShift - 2);
-            const uint32_t pos = gpos[b] + rk[k];
-            if (pos < lim[b]) pairs[pos] = make_uint2(w[k], sv[k]);
+        for (int k = 0; k < kItems; k++)
+            if ((putm >> k) & 1u) staged[lstart[w[k] >> (kSliceShift - 2)] + rk[k]] = make_uint2(w[k], sv[k]);
+        __syncthreads();
+        for (uint32_t i = t; i < total; i += kThreads) {
+            const uint2 p = staged[i];
+            const uint32_t b = p.x >> (kSliceShift - 2);
+            const uint32_t pos = gpos[b] + (i - lstart[b]);
+            if (pos < lim[b]) pairs[pos] = p;
         }
         if constexpr (MODE == kClamp) edge_add(fd, es);
         if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
@@ -221,11 +248,35 @@ __global__ void __launch_bounds__(kMaxSlices) k_scatter_scan(const unsigned *cnt
 
 // B: the placed updates in slice order.  word < words by construction (the
 // word offset of a fenced address of the partition); tested anyway, so
-// every address this kernel computes provably lies in the partition.
+// every address this kernel computes provably lies in the partition.  Each
+// CTA also prefetches into L2 (one bulk prefetch, cp.async.bulk.prefetch.L2)
+// its share of the NEXT updated slice, in proportion to its share of the
+// current one: the CTAs of a slice stream the following slice into L2 ahead
+// of its updates, so those REDs hit L2 and its lines are fetched (and later
+// written back) in address order rather than one random sector at a time.
 __global__ void __launch_bounds__(kThreads) k_scatter_apply(uint64_t base, uint64_t words, const uint2 *pairs,
-                                                            const unsigned *total) {
+                                                            const unsigned *total, const unsigned *cnt,
+                                                            const unsigned *lim) {
     const uint64_t n = *total;
-    const uint64_t i0 = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) * 4;
+    const uint64_t c0 = (uint64_t)blockIdx.x * kThreads * 4;
+    if (threadIdx.x == 0 && c0 < n) {
+        const uint32_t s = pairs[c0].x >> (kSliceShift - 2);             // the slice of the CTA's first update
+        const uint64_t e = lim[s], c = cnt[s], st = e - c;
+        const auto prefetch = [&](uint32_t sl, uint64_t from) {
+            const uint64_t lo = ((c0 - st) << kSliceShift) / c & ~127ull;
+            const uint64_t hi = (((c0 - st + (uint64_t)kThreads * 4) << kSliceShift) / c + 127) & ~127ull;
+            const uint64_t slice0 = (uint64_t)sl << kSliceShift, wbytes = words * 4;
+            uint64_t a = slice0 + lo, b = slice0 + (hi < (1ull << kSliceShift) ? hi : (1ull << kSliceShift));
+            if (b > wbytes) b = wbytes;
+            (void)from;
+            if (a < b)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + a), "r"((uint32_t)(b - a))
+                             : "memory");
+        };
+        if (st == 0) prefetch(s, st);                                    // the first slice: its own lines
+        if (e < n) prefetch(pairs[e].x >> (kSliceShift - 2), e);          // the next updated slice
+    }
+    const uint64_t i0 = c0 + (uint64_t)threadIdx.x * 4;
     if (i0 >= n) return;
     uint2 p[4];
     if (i0 + 4 <= n) {
@@ -275,7 +326,7 @@ cudaError_t bucketed_t(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64
         k_scatter_scan<<<1, kMaxSlices, 0, s>>>(cnt, cur, lim, total, nslices);
         k_scatter_part<MODE, 1><<<grid, kThreads, 0, s>>>(fd, table, idx, src, nvec, nslices, cnt, cur, lim, pairs);
         const unsigned gb = (unsigned)((4 * nvec + 4 * kThreads - 1) / (4 * kThreads));
-        k_scatter_apply<<<gb, kThreads, 0, s>>>(fd.base, fd.size / 4, pairs, total);
+        k_scatter_apply<<<gb, kThreads, 0, s>>>(fd.base, fd.size / 4, pairs, total, cnt, lim);
         e = cudaGetLastError();
     }
     const cudaError_t f = cudaFreeAsync(scratch, s);

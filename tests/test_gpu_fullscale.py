@@ -242,6 +242,7 @@ def test_c4_stencil_v2_full_sampled_rows(arenas):
     devmem.view(inp, H * W, torch.float32).uniform_(0, 1, generator=gen)
     devmem.view(out, H * W, torch.float32).fill_(-3.0)
     a.stencil_tma(p.id, "mask", out, inp, H, W, W, 0.5, 0.125)
+    assert a.device_flags() == 0                                       # no TMA wait expired
     rng = synth.rng_for(10)
     rows = np.concatenate([[1, 2, 16, 17, 18, H - 2], rng.integers(1, H - 1, 20)])
     for r in rows:

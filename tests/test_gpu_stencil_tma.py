@@ -15,6 +15,17 @@ ALL = ["none", "mask", "check", "modulo", "maskcount", "clamp"]
 FENCED = ALL[1:]
 
 
+@pytest.fixture(autouse=True)
+def no_tma_wait_timed_out():
+    """k_stencil_tma bounds its mbarrier waits (~2 s, then
+    it raises device flag bit 1 and stores nothing); after every K5 v2 test
+    the flags must be clear (no wait ever expired)."""
+    yield
+    from paper_2401_09290_b200 import guardian as g
+    with g.Arena(0, 1 << 20) as a:
+        assert a.device_flags() == 0
+
+
 @pytest.mark.parametrize("mode", ALL)
 @pytest.mark.parametrize("H,W,pitch", [(3, 3, 4), (67, 203, 208), (300, 1100, 1104), (130, 4, 4), (1030, 509, 512)])
 def test_stencil_tma_in_bounds(arenas, mode, H, W, pitch):

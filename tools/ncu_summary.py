@@ -76,6 +76,9 @@ def main():
                 key = (f"{mm.group(1)}<{mm.group(2).replace(' ', '')}>" if mm
                        else re.sub(r"^.*::", "", re.sub(r"\(.*", "", name)))
                 traffic[key] = rd + wr
+                if "dram__throughput.avg.pct_of_peak_sustained_elapsed" in d:
+                    traffic[key + ":dram_pct"] = d["dram__throughput.avg.pct_of_peak_sustained_elapsed"]["value"]
+                traffic["_source"] = f"ncu --set full, {os.path.basename(rep)}"
                 print(f"   traffic (dram read+write) = {rd + wr:.4e} B")
     if out:
         json.dump(summary, open(out, "w"), indent=1)
