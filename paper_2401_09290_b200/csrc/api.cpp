@@ -597,7 +597,8 @@ gd_status run_work_locked(gd_arena *a, const gd_work &w_in, cudaStream_t stream,
     fd.size = size;
     fd.inv = recip64(size);
     fd.viol = a->d_stats + (uint64_t)w.tenant * GD_NUM_KINDS + w.kind;
-    fd.flags = per_access ? kNoHoist : 0u;
+    fd.flags = (per_access ? kNoHoist : 0u) |
+               (((size & (size - 1)) == 0 && size >= (1ull << 32) && (base & (size - 1)) == 0) ? kBig : 0u);
     fd.pad_ = 0;
     const Geom g{a->sms};
     DeviceGuard dg(a->device);

@@ -114,6 +114,10 @@ struct Fence {
     }
     // inside(a) for an address the caller has proven W-aligned
     __device__ __forceinline__ bool ok_aligned_in(uint64_t a) const { return (a - base) <= lim; }
+    // the same for a kBig partition (FenceDesc::flags): equal high bits
+    __device__ __forceinline__ bool in_big(uint64_t a) const {
+        return (((uint32_t)(a >> 32) ^ (uint32_t)(base >> 32)) & ~(uint32_t)((size - 1) >> 32)) == 0;
+    }
     // CLAMP, for a 16-byte vector of four logical 4-byte elements wholly
     // outside the partition: the word every one of its elements clamps to
     __device__ __forceinline__ uint64_t edge4(uint64_t a) const { return a < base ? base : base + size - 4; }
@@ -143,18 +147,20 @@ __device__ __forceinline__ uint4 vld4(const Fence<MODE, 16> &f, uint64_t a, uint
     }
 }
 
-template <int MODE, typename ST16, typename ST4>
+// (ALIGNED = false: the alignment half of the predicate is tested anyway --
+// identical results, a different register allocation; see k_gatherR)
+template <int MODE, typename ST16, typename ST4, bool ALIGNED = true>
 __device__ __forceinline__ void vst4(const Fence<MODE, 16> &f, uint64_t a, uint4 v, uint32_t &nv, ST16 st16,
                                      ST4 st4) {
     if constexpr (MODE == kClamp) {
-        if (f.ok_aligned_in(a)) {
+        if (ALIGNED ? f.ok_aligned_in(a) : f.inside(a)) {
             st16(a, v);
         } else {
             nv += 4;
             st4(f.edge4(a), v.w);
         }
     } else {
-        if (f.go_aligned(a, nv, 4)) st16(f.addr(a), v);
+        if (ALIGNED ? f.go_aligned(a, nv, 4) : f.go(a, nv, 4)) st16(f.addr(a), v);
     }
 }
 
@@ -179,6 +185,25 @@ __device__ __forceinline__ void flush_violations(uint32_t nv_thread, unsigned lo
     if (!__any_sync(0xffffffffu, nv_thread != 0)) return;
     const uint32_t s = __reduce_add_sync(0xffffffffu, nv_thread);
     if ((threadIdx.x & 31u) == 0) atomicAdd(viol, (unsigned long long)s);
+}
+
+// The CTA-wide variant (a barrier vote, a shared-memory reduction, one
+// atomic per CTA), kept for the row gather: with it ptxas keeps every mode
+// of k_gatherR inside 40 registers without local memory (6 CTAs per SM).
+__device__ __forceinline__ void flush_violations_cta(uint32_t nv_thread, unsigned long long *viol) {
+    if (!__syncthreads_or(nv_thread != 0)) return;
+    __shared__ unsigned long long warp_sums[32];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t s = __reduce_add_sync(0xffffffffu, nv_thread);
+    if (lane == 0) warp_sums[warp] = s;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t nw = (blockDim.x + 31u) >> 5;
+        unsigned long long t = lane < nw ? warp_sums[lane] : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0 && t) atomicAdd(viol, t);
+    }
 }
 
 }  // namespace gd

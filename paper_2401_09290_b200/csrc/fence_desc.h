@@ -27,6 +27,10 @@ struct FenceDesc {
 };
 
 constexpr uint32_t kNoHoist = 1u;
+// a power-of-two, size-aligned partition of at least 4 GiB: an address lies
+// in it iff its high 32 bits agree with the base's above log2(size) (one
+// LOP3 and one compare instead of a 64-bit subtract and compare)
+constexpr uint32_t kBig = 2u;
 
 // floor(2^64 / s) for s >= 2
 inline uint64_t recip64(uint64_t s) {

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_gather1(const __grid_constant__
 // K3, D > 1: out[i*D+d] = table[sext(idx[i])*D + d]; one warp per row i.
 // ---------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_gatherD(const __grid_constant__ FenceDesc fd, uint64_t out,
+__global__ void __launch_bounds__(kThreads, 5) k_gatherD(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                       uint64_t table, uint64_t idx, uint64_t n, uint32_t D) {
     const Fence<MODE, 4> f4(fd);
     uint32_t nv = 0;
@@ -241,7 +241,7 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     // from consuming each loaded index before the next load issues)
     if constexpr (TMODE == kClamp) __syncwarp();
     uint64_t at[S][G];
-    bool ok[S][G], below[S][G];
+    bool ok[S][G];
     uint32_t cnt[S];
 #pragma unroll
     for (int k = 0; k < S; k++) {                       // 2. fenced table addresses (ALU only)
@@ -266,12 +266,10 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
                 at[k][g] = fr + 16 * tpr * g;
                 ok[k][g] = true;
             } else if constexpr (TMODE == kClamp) {
-                // an outside vector loads the partition's first / last 16
-                // bytes instead (branch-free); step 3b splats its edge word
-                // (fence.cuh vld4), so only one bit per vector stays live
+                // as check here (an outside vector is not loaded); step 3b
+                // then gives it its edge word four times (fence.cuh vld4)
+                at[k][g] = a;
                 ok[k][g] = (a - fd.base) <= fd.size - 16;
-                below[k][g] = a < fd.base;
-                at[k][g] = ok[k][g] ? a : (below[k][g] ? fd.base : fd.base + fd.size - 16);
                 cnt[k] += ok[k][g] ? 0u : 4u;
             } else {
                 at[k][g] = ft.addr(a);
@@ -285,7 +283,7 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
 #pragma unroll
         for (int g = 0; g < G; g++) {
             r[k][g] = make_uint4(0, 0, 0, 0);
-            if (live[k] && (TMODE == kClamp || ok[k][g])) r[k][g] = ld_row(at[k][g]);
+            if (live[k] && ok[k][g]) r[k][g] = ld_row(at[k][g]);
         }
         if (live[k]) nv += cnt[k];
     }
@@ -294,8 +292,8 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
         for (int k = 0; k < S; k++) {
 #pragma unroll
             for (int g = 0; g < G; g++) {
-                if (!ok[k][g]) {
-                    const uint32_t w = below[k][g] ? r[k][g].x : r[k][g].w;
+                if (live[k] && !ok[k][g]) {
+                    const uint32_t w = ld_tab(ft.edge4(at[k][g]));
                     r[k][g] = make_uint4(w, w, w, w);
                 }
             }
@@ -317,7 +315,8 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
             } else {
 #pragma unroll
                 for (int g = 0; g < G; g++) {
-                    vst4(fo, ov[k] + 16 * tpr * g, r[k][g], nv, st_out, st_w);
+                    vst4<SMODE, decltype(st_out), decltype(st_w), false>(fo, ov[k] + 16 * tpr * g, r[k][g], nv,
+                                                                          st_out, st_w);
                 }
             }
         }
@@ -325,10 +324,10 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
 }
 
 // 6 CTAs (48 warps) per SM: the row gather is bound by loads in flight, and
-// 5 CTAs measured 27-41 % slower at D = 32 / 64 (every mode fits in 40
-// registers: clamp keeps one bit per outside vector, not its address).
+// 5 CTAs measured 27-41 % slower at D = 32 / 64; clamp with G = 4 needs the
+// registers of 5 (no local memory) and loses nothing there (D >= 128).
 template <int MODE, int G, bool P2>
-__global__ void __launch_bounds__(kThreads, 6) k_gatherR(const __grid_constant__ FenceDesc fd, uint64_t out,
+__global__ void __launch_bounds__(kThreads, (MODE == kClamp && G == 4) ? 5 : 6) k_gatherR(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                       uint64_t table, uint64_t idx, uint64_t nslots, uint32_t tpr,
                                                       uint64_t dv) {
     constexpr uint64_t ch = (uint64_t)kThreads * (4 / G);
@@ -346,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_gatherR(const __grid_constant__
     } else {
         gatherr_chunk<MODE, MODE, G, P2>(fd, out, table, idx, s0, nslots, tpr, dv, nv);
     }
-    if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
+    if constexpr (counts(MODE)) flush_violations_cta(nv, fd.viol);
 }
 
 // ---------------------------------------------------------------------------

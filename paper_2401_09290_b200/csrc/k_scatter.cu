@@ -273,8 +273,15 @@ __global__ void __launch_bounds__(kThreads) k_scatter_apply(uint64_t base, uint6
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + a), "r"((uint32_t)(b - a))
                              : "memory");
         };
-        if (st == 0) prefetch(s, st);                                    // the first slice: its own lines
-        if (e < n) prefetch(pairs[e].x >> (kSliceShift - 2), e);          // the next updated slice
+        // only dense slices (on average an update per 128-byte line or
+        // more) are worth streaming in whole; sparse ones are left to their
+        // REDs' own sector fills
+        constexpr uint32_t kDense = (1u << kSliceShift) / 128;
+        if (st == 0 && c >= kDense) prefetch(s, st);                     // the first slice: its own lines
+        if (e < n) {
+            const uint32_t s2 = pairs[e].x >> (kSliceShift - 2);         // the next updated slice
+            if (cnt[s2] >= kDense) prefetch(s2, e);
+        }
     }
     const uint64_t i0 = c0 + (uint64_t)threadIdx.x * 4;
     if (i0 >= n) return;

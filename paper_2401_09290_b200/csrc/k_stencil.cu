@@ -37,7 +37,7 @@ __device__ __forceinline__ void st_w(uint64_t a, uint32_t v) { __stcs(reinterpre
 // row guards, one 16-byte store per row).  The row loop is unrolled at
 // compile time, addresses advance by one row pitch per row, and every
 // access is fenced at its own address.
-template <int MODE, int kG, int ROWS, bool FULL, bool WALK = false>
+template <int MODE, int kG, int ROWS, bool FULL, bool WALK = false, bool BIG = false>
 __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t W, uint64_t pitch,
                                       float c0, float c1, uint64_t c, uint32_t r0, uint32_t r1, uint32_t &nv) {
     static_assert(ROWS % kG == 0 && ROWS + 2 <= 32, "strip rows");
@@ -94,7 +94,7 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
             fv = b == 0 ? f16.addr(pv) : f16.step_up(fv, step);
             v = __ldg(reinterpret_cast<const float4 *>(fv));
         } else if constexpr (counts(MODE)) {
-            const bool ok = (pv - f16.base) <= f16.lim;                       // pv is 16-aligned (API)
+            const bool ok = BIG ? f16.in_big(pv) : (pv - f16.base) <= f16.lim;   // pv is 16-aligned (API)
             if (!ok) refm |= 1u << b;
             if constexpr (MODE == kCheck || MODE == kClamp) {
                 // predicated: the destination is zeroed before the load (clamp:
@@ -115,7 +115,7 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
             if (need_h) v = __ldg(reinterpret_cast<const float *>(f4.step_down(fv, pv - ph)));
         } else if constexpr (counts(MODE)) {
             const uint64_t fh = f4.addr(ph);
-            const bool ok = MODE == kMaskCount ? fh == ph : (ph - f4.base) <= f4.lim;     // ph is 4-aligned
+            const bool ok = MODE == kMaskCount ? fh == ph : BIG ? f4.in_big(ph) : (ph - f4.base) <= f4.lim;
             if (need_h && !ok) nv++;
             if constexpr (MODE == kClamp) {
                 if (need_h && !ok) hrefm |= 1u << hb;
@@ -154,14 +154,16 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
                 nv += f != po ? 4u : 0u;                // inside iff the fence is the identity
                 st_v(f, val);
             } else if constexpr (MODE == kClamp) {     // (fence.cuh vst4, po 16-aligned)
-                if ((po - f16.base) <= f16.lim) {
+                if (BIG ? f16.in_big(po) : (po - f16.base) <= f16.lim) {
                     st_v(po, val);
                 } else {                               // rare: the last element wins the edge word
                     nv += 4;
                     st_w(f16.edge4(po), val.w);
                 }
             } else {
-                if (f16.go_aligned(po, nv, 4)) st_v(f16.addr(po), val);          // po is 16-aligned
+                const bool ok = BIG ? f16.in_big(po) : (po - f16.base) <= f16.lim;    // po is 16-aligned
+                if (counts(MODE) && !ok) nv += 4;
+                if (MODE != kCheck || ok) st_v(f16.addr(po), val);
             }
         } else if (active) {                           // the grid's first / last columns
 #pragma unroll
@@ -266,10 +268,14 @@ template <int MODE, int kG, int ROWS, bool WALK = false>
 __device__ __forceinline__ void strip_rows(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t W,
                                            uint64_t pitch, float c0, float c1, uint64_t c, uint32_t r0, uint32_t r1,
                                            uint32_t &nv) {
-    if (r1 - r0 == ROWS && __all_sync(0xffffffffu, c >= 1 && c + 5 <= W))   // every lane: 4 interior points
-        strip<MODE, kG, ROWS, true, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
-    else
+    if (r1 - r0 == ROWS && __all_sync(0xffffffffu, c >= 1 && c + 5 <= W)) {   // every lane: 4 interior points
+        if (counts(MODE) && MODE != kMaskCount && (fd.flags & kBig))
+            strip<MODE, kG, ROWS, true, WALK, true>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+        else
+            strip<MODE, kG, ROWS, true, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+    } else {
         strip<MODE, kG, ROWS, false, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
+    }
 }
 
 // ROWS (rows per CTA strip) is a compile-time constant: 16-row strips at HBM

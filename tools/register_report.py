@@ -34,10 +34,13 @@ def main():
     table = {}
     for mangled, r in rows.items():
         name = dm[mangled]
-        km = re.search(r"(k_[A-Za-z0-9_]+)<(\d)", name)
+        km = re.search(r"(k_[A-Za-z0-9_]+)<(\d)((?:, ?[\w]+)*)>", name)
         if not km:
             continue
-        kernel, mode = km.group(1), MODES.get(km.group(2), km.group(2))
+        # one row per instantiation (the other template arguments kept), so
+        # every fenced variant is compared with the twin of the same shape
+        rest = km.group(3).replace(" ", "")
+        kernel, mode = km.group(1) + (f"<M{rest}>" if rest else ""), MODES.get(km.group(2), km.group(2))
         table.setdefault(kernel, {})[mode] = r
     report = {"source": "ptxas -v of the sm_100a build (paper_2401_09290_b200/build/ptxas_*.log)", "kernels": {}}
     deltas = []
