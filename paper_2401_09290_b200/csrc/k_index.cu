@@ -180,8 +180,14 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     // Phases keep every load of a kind in flight together: the fence's rare
     // per-vector path is a branch, and a branch between two loads would
     // serialise their latencies.
-    bool live[S];
+    bool live[S], okj[S];
     int32_t j[S];
+    // A refused (or dead) index load reads a safe word instead -- the first
+    // index of the launch when the streams are unfenced, else the partition's
+    // base -- and its value is replaced by 0 only where it is used (step 2):
+    // a predicated load would make the compiler consume each loaded index
+    // (its sign extension) before the next load issues.
+    const uint64_t safe = SMODE == kNone ? idx : fd.base;
     uint64_t ov[S], tv[S];
     // Per-access modulo on the streams (SMODE == kModulo: hoisting off): this
     // thread's index and output addresses increase with k (and g), so when
@@ -211,11 +217,11 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
             const uint64_t ai = idx + 4 * i;
             uint32_t ci = 0;
             const bool oki = fi.go_aligned(ai, ci, 1) && live[k];        // ALU only: no branch
-            j[k] = 0;
             const uint64_t fa = (k == 0 || !walk) ? fi.addr(ai) : fi.step_up(fa_prev, ai - aa_prev);
             fa_prev = fa;
             aa_prev = ai;
-            if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fa));
+            okj[k] = oki;
+            j[k] = __ldg(reinterpret_cast<const int32_t *>(oki ? fa : safe));
             if (live[k] && t == 0) nv += ci;                             // one index access per row
             ov[k] = out + 16 * (i * vpr + t);
             tv[k] = 16 * t;
@@ -230,8 +236,13 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
             const uint64_t ai = idx + 4 * i;
             uint32_t ci = 0;
             const bool oki = fi.go_aligned(ai, ci, 1) && live[k];        // ALU only: no branch
-            j[k] = 0;
-            if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fi.addr(ai)));
+            okj[k] = oki;
+            if constexpr (SMODE == kClamp) {            // (clamp: only dead slots are refused)
+                j[k] = 0;
+                if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fi.addr(ai)));
+            } else {
+                j[k] = __ldg(reinterpret_cast<const int32_t *>(oki ? fi.addr(ai) : safe));
+            }
             if (live[k] && t == 0) nv += ci;                             // one index access per row
             ov[k] = out + 16 * (i * vpr + t);
             tv[k] = 16 * t;
@@ -245,7 +256,8 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     uint32_t cnt[S];
 #pragma unroll
     for (int k = 0; k < S; k++) {                       // 2. fenced table addresses (ALU only)
-        const uint64_t rt = table + (uint64_t)((int64_t)j[k] * (int64_t)rowbytes) + tv[k];   // vector g = 0
+        const int32_t jk = (SMODE == kClamp || okj[k]) ? j[k] : 0;   // a refused index load reads 0
+        const uint64_t rt = table + (uint64_t)((int64_t)jk * (int64_t)rowbytes) + tv[k];   // vector g = 0
         bool whole = false;                             // every vector of the slot in / unwrapped
         uint64_t fr = rt;
         cnt[k] = 0;

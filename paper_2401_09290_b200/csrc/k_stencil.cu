@@ -46,7 +46,10 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
     const Fence<MODE, 16> f16(fd);
     const Fence<MODE, 4> f4(fd);
     const uint32_t lane = threadIdx.x & 31u;
-    const bool active = FULL || c < W;
+#ifndef GD_STENCIL_FULL_WARP
+#define GD_STENCIL_FULL_WARP 1
+#endif
+    const bool active = (FULL && GD_STENCIL_FULL_WARP) || c < W;
     bool interior[4];
     bool all4 = true;
 #pragma unroll
@@ -54,7 +57,7 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         interior[k] = (c + k >= 1) && (c + k + 2 <= W);
         all4 = all4 && interior[k];
     }
-    const bool all4a = FULL || all4;                   // (all four interior implies c < W)
+    const bool all4a = (FULL && GD_STENCIL_FULL_WARP) || all4;   // (all four interior implies c < W)
     // The W word of point k = 0 (column c-1) is word 3 of lane-1's vector of
     // the same row, the E word of point k = 3 (column c+4) word 0 of
     // lane+1's: F4(a-4) = F16(a-16)+12 and F4(a+16) = F16(a+16) in every
@@ -268,7 +271,7 @@ template <int MODE, int kG, int ROWS, bool WALK = false>
 __device__ __forceinline__ void strip_rows(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t W,
                                            uint64_t pitch, float c0, float c1, uint64_t c, uint32_t r0, uint32_t r1,
                                            uint32_t &nv) {
-    if (r1 - r0 == ROWS && __all_sync(0xffffffffu, c >= 1 && c + 5 <= W)) {   // every lane: 4 interior points
+    if (r1 - r0 == ROWS && (!GD_STENCIL_FULL_WARP || __all_sync(0xffffffffu, c >= 1 && c + 5 <= W))) {
         if (counts(MODE) && MODE != kMaskCount && (fd.flags & kBig))
             strip<MODE, kG, ROWS, true, WALK, true>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
         else
@@ -309,7 +312,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil(const __grid_constant__
     } else {
         strip_rows<MODE, 4, ROWS>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
     }
+#ifdef GD_STENCIL_CTA_FLUSH
+    if constexpr (counts(MODE)) flush_violations_cta(nv, fd.viol);
+#else
     if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
+#endif
 }
 
 // Per-access fencing (GD_FENCE_PER_ACCESS, fd.flags & kNoHoist, the paper's
@@ -342,7 +349,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_stencil_pa(const __grid_constan
     } else {
         strip_rows<MODE, 4, ROWS>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
     }
+#ifdef GD_STENCIL_CTA_FLUSH
+    if constexpr (counts(MODE)) flush_violations_cta(nv, fd.viol);
+#else
     if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
+#endif
 }
 
 template <int MODE>

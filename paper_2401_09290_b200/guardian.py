@@ -14,7 +14,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libguardian.so")
+# GD_LIB: a development build of the same library (tools/ A/B probes only)
+LIB_PATH = os.environ.get("GD_LIB") or os.path.join(_PKG, "libguardian.so")
 
 GD_OK = 0
 STATUS = ["GD_OK", "GD_ERR_INVALID_ARG", "GD_ERR_NOT_POW2", "GD_ERR_DEVICE_OOM", "GD_ERR_PARTITION_OOM",
