@@ -36,6 +36,15 @@ GiB = 1 << 30
 MiB = 1 << 20
 # fence modes in gd_mode order; the unfenced twin first (overheads are against it)
 ALL_MODES = ("none", "mask", "check", "modulo", "maskcount", "clamp")
+
+
+def rotated(modes, r):
+    """The mode order of repetition r: rotated by r, so that over len(modes)
+    repetitions every mode runs once in every position of the sequence (a
+    kernel's clock under the power cap depends on what ran just before it;
+    a fixed order biased the later modes of the 0.5 ms GEMM by up to 5 %)."""
+    k = r % len(modes)
+    return list(modes[k:]) + list(modes[:k])
 TENANTS = 8
 PART = 1 << 34                    # 16 GiB
 ARENA = TENANTS * PART            # 2^37
@@ -401,8 +410,8 @@ class Workload:
             with torch.cuda.stream(s):
                 for m in modes:
                     fn(launch_mode[m], s)
-                for _ in range(reps):
-                    for m in modes:
+                for r in range(reps):
+                    for m in rotated(modes, r):
                         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         e0.record(s)
                         fn(launch_mode[m], s)
@@ -474,8 +483,8 @@ class Workload:
                     graphs[m] = gr
                 for m in modes:
                     graphs[m].replay()
-                for _ in range(reps):
-                    for m in modes:
+                for r in range(reps):
+                    for m in rotated(modes, r):
                         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                         e0.record(s)
                         graphs[m].replay()
@@ -605,8 +614,8 @@ def run_gpu(args):
     # ---- overhead vs the unfenced twin: every mode, interleaved ----
     modes = ALL_MODES
     per_mode = {m: [] for m in modes}
-    for _ in range(args.reps):
-        for m in modes:
+    for r in range(args.reps):
+        for m in rotated(modes, r):
             per_mode[m].append(allreduce([w.time_steps(m, args.steps)])[0] / args.steps)
     med = {m: statistics.median(v) for m, v in per_mode.items()}
     modes_gbs = {m: round(world * STEP_BYTES_PER_GPU / (med[m] / 1e3) / 1e9, 1) for m in med}
@@ -1049,13 +1058,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--mode", default="mask", choices=list(ALL_MODES))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--reps", type=int, default=5, help="interleaved none/mask/check repetitions")
+    ap.add_argument("--reps", type=int, default=6, help="interleaved repetitions of the six modes (rotated order)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the mixed multi-tenant (configs[4]) measurement")
     ap.add_argument("--c5-launches", type=int, default=20)
-    ap.add_argument("--table-reps", type=int, default=5)
+    ap.add_argument("--table-reps", type=int, default=6, help="a multiple of 6: every mode once in every position")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--dry-run", action="store_true",
                     help="the rank plumbing on CPU: gloo, virtual arenas, validation only, no kernels")

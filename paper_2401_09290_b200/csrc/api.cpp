@@ -150,6 +150,33 @@ bool tenant_live(gd_arena *a, uint32_t id) {
     return id < GD_MAX_TENANTS && a->parts[id].live;
 }
 
+// The trusted device memory of an arena, one cudaMalloc outside it (SURVEY
+// H9): the violation counters u64[GD_MAX_TENANTS][GD_NUM_KINDS], then a
+// 256-byte all-zero block that refused check-mode loads read (FenceDesc::zero;
+// nothing ever writes it).  Zeroed; synchronises.
+constexpr uint64_t kStatsBytes = sizeof(unsigned long long) * GD_MAX_TENANTS * GD_NUM_KINDS;
+constexpr uint64_t kZeroOff = (kStatsBytes + 255) & ~255ull, kTrustedBytes = kZeroOff + 256;
+
+gd_status alloc_trusted(gd_arena *a) {
+    void *st = nullptr;
+    cudaError_t e = cudaMalloc(&st, kTrustedBytes);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const uint64_t sp = (uint64_t)st, se = sp + kTrustedBytes;
+    if (se > a->base && sp < a->base + a->size) {        // H9: never inside the arena
+        cudaFree(st);
+        return GD_ERR_INVALID_ARG;
+    }
+    e = cudaMemset(st, 0, kTrustedBytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(st);
+        return cuda_fail(e);
+    }
+    a->d_stats = (unsigned long long *)st;
+    a->d_zero = sp + kZeroOff;
+    return GD_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -189,24 +216,12 @@ extern "C" gd_status gd_arena_create(int device, uint64_t bytes, uint32_t flags,
     a->size = bytes;
     a->buddy.init(bytes, 12);
     cudaDeviceGetAttribute(&a->sms, cudaDevAttrMultiProcessorCount, device);
-    void *st = nullptr;
-    cudaError_t e = cudaMalloc(&st, sizeof(unsigned long long) * GD_MAX_TENANTS * GD_NUM_KINDS);
-    if (e != cudaSuccess) {
+    const gd_status ts = alloc_trusted(a);
+    if (ts != GD_OK) {
         d.MemAddressFree(va, reserve);
         delete a;
-        return cuda_fail(e);
+        return ts;
     }
-    // H9: the trusted counters must not lie inside the arena
-    const uint64_t sp = (uint64_t)st, se = sp + sizeof(unsigned long long) * GD_MAX_TENANTS * GD_NUM_KINDS;
-    if (se > a->base && sp < a->base + a->size) {
-        cudaFree(st);
-        d.MemAddressFree(va, reserve);
-        delete a;
-        return GD_ERR_INVALID_ARG;
-    }
-    a->d_stats = (unsigned long long *)st;
-    cudaMemset(st, 0, sizeof(unsigned long long) * GD_MAX_TENANTS * GD_NUM_KINDS);
-    cudaDeviceSynchronize();
     *out = a;
     return GD_OK;
 }
@@ -230,21 +245,11 @@ extern "C" gd_status gd_arena_wrap(int device, uint64_t dev_ptr, uint64_t bytes,
             return cuda_fail(dg.err);
         }
         cudaDeviceGetAttribute(&a->sms, cudaDevAttrMultiProcessorCount, device);
-        void *st = nullptr;
-        cudaError_t e = cudaMalloc(&st, sizeof(unsigned long long) * GD_MAX_TENANTS * GD_NUM_KINDS);
-        if (e != cudaSuccess) {
+        const gd_status ts = alloc_trusted(a);
+        if (ts != GD_OK) {
             delete a;
-            return cuda_fail(e);
+            return ts;
         }
-        const uint64_t sp = (uint64_t)st, se = sp + sizeof(unsigned long long) * GD_MAX_TENANTS * GD_NUM_KINDS;
-        if (se > a->base && sp < a->base + a->size) {
-            cudaFree(st);
-            delete a;
-            return GD_ERR_INVALID_ARG;
-        }
-        a->d_stats = (unsigned long long *)st;
-        cudaMemset(st, 0, sizeof(unsigned long long) * GD_MAX_TENANTS * GD_NUM_KINDS);
-        cudaDeviceSynchronize();
     }
     *out = a;
     return GD_OK;
@@ -599,6 +604,7 @@ gd_status run_work_locked(gd_arena *a, const gd_work &w_in, cudaStream_t stream,
     fd.viol = a->d_stats + (uint64_t)w.tenant * GD_NUM_KINDS + w.kind;
     fd.flags = (per_access ? kNoHoist : 0u) |
                (((size & (size - 1)) == 0 && size >= (1ull << 32) && (base & (size - 1)) == 0) ? kBig : 0u);
+    fd.zero = a->d_zero;
     fd.pad_ = 0;
     const Geom g{a->sms};
     DeviceGuard dg(a->device);

@@ -79,6 +79,7 @@ struct gd_arena {
     gd::Partition parts[GD_MAX_TENANTS];
     gd::HostCounters host[GD_MAX_TENANTS][GD_NUM_KINDS];
     unsigned long long *d_stats = nullptr;  // u64[GD_MAX_TENANTS][GD_NUM_KINDS], outside the arena
+    uint64_t d_zero = 0;             // trusted all-zero 256-byte block after the counters (FenceDesc::zero)
     void *zero_buf = nullptr;        // trusted zero row for operands with no rows (gemm.cu)
     uint64_t zero_bytes = 0;
     std::vector<void *> zero_retired;  // outgrown zero rows: captured graphs may still read them (freed at destroy)

@@ -33,15 +33,29 @@
 
 #include "fence_desc.h"
 
+// Refused check / clamp loads read the trusted zero block (Fence::ld_at)
+// instead of being predicated off; 0 restores predicated loads (A/B builds).
+#ifndef GD_ZERO_REDIRECT
+#define GD_ZERO_REDIRECT 1
+#endif
+
 namespace gd {
 
 // Per-width precomputation, hoisted out of every loop (uniform values).
 template <int MODE, int W>
 struct Fence {
-    uint64_t base, keep, size, inv, lim;
+    uint64_t base, keep, size, inv, lim, zero;
+    uint32_t mask_hi;              // high word of size - 1 (= of keep for every W <= 16)
     __device__ __forceinline__ explicit Fence(const FenceDesc &fd)
         : base(fd.base), keep(W == 16 ? fd.mask16 : W == 4 ? fd.mask4 : fd.mask & ~(uint64_t)(W - 1)), size(fd.size),
-          inv(fd.inv), lim(fd.size - W) {}
+          inv(fd.inv), lim(fd.size - W), zero(fd.zero), mask_hi((uint32_t)(fd.mask >> 32)) {}
+    // The address a load reads when `ok` may refuse it (check / clamp
+    // predicate, or a dead lane): refused -> the trusted zero block, which
+    // reads 0 exactly as a refused check-mode load must (reading A1).  An
+    // unpredicated load from a selected address keeps every load of a batch
+    // free of predicates (a predicated load's destination must be zeroed
+    // first and ties the scheduler to that order).  W <= 16.
+    __device__ __forceinline__ uint64_t ld_at(uint64_t a, bool ok) const { return ok ? a : zero; }
     // address the access really uses (MASK / MODULO / CLAMP: fenced; CHECK / NONE: unchanged)
     __device__ __forceinline__ uint64_t addr(uint64_t a) const {
         if constexpr (MODE == kMask || MODE == kMaskCount) {
@@ -111,6 +125,16 @@ struct Fence {
         } else {
             return true;
         }
+    }
+    // MASK / MASK_COUNT on a kBig partition (FenceDesc::flags: power of two,
+    // >= 4 GiB, size-aligned, so base's low word is 0 and keep's low word is
+    // all ones above the W alignment) for a W-aligned address: the fence
+    // leaves the low word as it is, so it is one LOP3 on the high word --
+    // equal to addr(a).  The high words of keep and base are the same for
+    // every W, so the 4- and 16-byte fences of a kernel share their operands.
+    __device__ __forceinline__ uint64_t addr_big(uint64_t a) const {
+        const uint32_t hi = ((uint32_t)(a >> 32) & mask_hi) | (uint32_t)(base >> 32);
+        return ((uint64_t)hi << 32) | (uint64_t)(uint32_t)a;
     }
     // inside(a) for an address the caller has proven W-aligned
     __device__ __forceinline__ bool ok_aligned_in(uint64_t a) const { return (a - base) <= lim; }

@@ -22,6 +22,8 @@ struct FenceDesc {
     uint64_t size;                 // partition size in bytes (check / modulo)
     uint64_t inv;                  // floor(2^64 / size): modulo-mode reciprocal
     unsigned long long *viol;      // trusted counter (outside every partition)
+    uint64_t zero;                 // trusted all-zero 256-byte block outside every partition: a load the
+                                   // check predicate refuses reads here instead (it reads 0, reading A1)
     uint32_t flags;                // kNoHoist: check / modulo fence every access (no tile-level range test)
     uint32_t pad_;
 };

@@ -39,8 +39,13 @@ __device__ __forceinline__ uint64_t row_addr(uint64_t table, int32_t j) {
 template <int MODE>
 __device__ __forceinline__ uint32_t fenced_tab(const Fence<MODE, 4> &f4, uint64_t table, int32_t j, uint32_t &nv) {
     const uint64_t a = row_addr(table, j);
+#if GD_ZERO_REDIRECT
+    const bool o = f4.go(a, nv, 1);
+    return ld_tab(f4.ld_at(f4.addr(a), o));           // refused: the trusted zero block
+#else
     if (f4.go(a, nv, 1)) return ld_tab(f4.addr(a));
     return 0u;
+#endif
 }
 
 __device__ __forceinline__ uint64_t chunk_len(uint64_t nvec, uint64_t c0) {
@@ -150,6 +155,25 @@ __global__ void __launch_bounds__(kThreads, 5) k_gatherD(const __grid_constant__
 // Logical accesses as in the oracle: one index load per row (counted by the
 // row's t == 0 slot), D table loads and D stores per row (4 per vector).
 // ---------------------------------------------------------------------------
+// Code-generation choices of the row gather, measured per access at 1 GiB
+// of gathered rows (tools/r02_iter5.sh; A/B with tools/build_variant.sh):
+// CLAMP_SAFE: clamp's index loads read a safe word when the slot is dead, as
+//   the other modes do (G = 1 with a power-of-two slot count, e.g. D = 32:
+//   +8.4 -> -0.5 %; the non-power-of-two row index would spill; G >= 2 kept
+//   predicated: D = 64 +5.8 -> +11.3 %, and G = 4 would spill);
+// LIVE_REDIRECT: a dead slot's table vector is read from the trusted zero
+//   block in none / mask / mask-count too, instead of a predicated load
+//   (mask-count D = 64: +13.2 -> +0.3 %; modulo and clamp keep the
+//   predicated load: 7-40 % slower with the selected address).
+#ifndef GD_GATHER_CLAMP_SAFE
+#define GD_GATHER_CLAMP_SAFE 1
+#endif
+#ifndef GD_GATHER_CLAMP_SYNCWARP
+#define GD_GATHER_CLAMP_SYNCWARP 1
+#endif
+#ifndef GD_GATHER_LIVE_REDIRECT
+#define GD_GATHER_LIVE_REDIRECT 1
+#endif
 // Row of slot sl without a branch (a branch between the index loads would
 // make the compiler consume each loaded index before the next load issues):
 // a shift when the slots per row are a power of two (P2, dv = log2 tpr),
@@ -237,7 +261,7 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
             uint32_t ci = 0;
             const bool oki = fi.go_aligned(ai, ci, 1) && live[k];        // ALU only: no branch
             okj[k] = oki;
-            if constexpr (SMODE == kClamp) {            // (clamp: only dead slots are refused)
+            if constexpr (SMODE == kClamp && !(GD_GATHER_CLAMP_SAFE && G == 1 && P2)) {   // (clamp: only dead slots are refused)
                 j[k] = 0;
                 if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fi.addr(ai)));
             } else {
@@ -250,13 +274,13 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     }
     // (clamp: a warp-synchronising point after the index loads keeps ptxas
     // from consuming each loaded index before the next load issues)
-    if constexpr (TMODE == kClamp) __syncwarp();
+    if constexpr (TMODE == kClamp && GD_GATHER_CLAMP_SYNCWARP) __syncwarp();
     uint64_t at[S][G];
     bool ok[S][G];
     uint32_t cnt[S];
 #pragma unroll
     for (int k = 0; k < S; k++) {                       // 2. fenced table addresses (ALU only)
-        const int32_t jk = (SMODE == kClamp || okj[k]) ? j[k] : 0;   // a refused index load reads 0
+        const int32_t jk = ((SMODE == kClamp && !(GD_GATHER_CLAMP_SAFE && G == 1 && P2)) || okj[k]) ? j[k] : 0;   // a refused index load reads 0
         const uint64_t rt = table + (uint64_t)((int64_t)jk * (int64_t)rowbytes) + tv[k];   // vector g = 0
         bool whole = false;                             // every vector of the slot in / unwrapped
         uint64_t fr = rt;
@@ -294,8 +318,16 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     for (int k = 0; k < S; k++) {                       // 3. table loads
 #pragma unroll
         for (int g = 0; g < G; g++) {
-            r[k][g] = make_uint4(0, 0, 0, 0);
-            if (live[k] && ok[k][g]) r[k][g] = ld_row(at[k][g]);
+            if constexpr (GD_ZERO_REDIRECT && (TMODE == kCheck || (GD_GATHER_LIVE_REDIRECT && (TMODE == kNone ||
+                                                  TMODE == kMask || TMODE == kMaskCount)))) {
+                // refused / dead: the trusted zero block (per access at D = 32:
+                // +3.8 -> +1.1 %; the predicated form stays for the other
+                // modes, where the selected address measured 7-40 % slower)
+                r[k][g] = ld_row(ft.ld_at(at[k][g], live[k] && ok[k][g]));
+            } else {
+                r[k][g] = make_uint4(0, 0, 0, 0);
+                if (live[k] && ok[k][g]) r[k][g] = ld_row(at[k][g]);
+            }
         }
         if (live[k]) nv += cnt[k];
     }

@@ -45,6 +45,23 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
     // a lane past the grid's width (c >= W) loads nothing and stores nothing.
     const Fence<MODE, 16> f16(fd);
     const Fence<MODE, 4> f4(fd);
+    // the mask fence of a 16- / 4-aligned address (BIG: one LOP3, Fence::addr_big)
+    constexpr bool kMaskBig = BIG && (MODE == kMask || MODE == kMaskCount);
+    auto fa16 = [&](uint64_t a) { return kMaskBig ? f16.addr_big(a) : f16.addr(a); };
+    auto fa4 = [&](uint64_t a) { return kMaskBig ? f4.addr_big(a) : f4.addr(a); };
+    // CHECK on a kBig partition: every load is issued, unpredicated, at its
+    // mask-fenced address (inside the tenant's own partition), and a refused
+    // load's value is replaced by 0 after its batch of loads (zerofix below,
+    // the rare path): the values used are exactly the check fence's (refused
+    // -> 0) and nothing outside the partition is read.  A predicated load ties
+    // each destination to a zeroing move and let ptxas start the next batch
+    // only after the previous one was consumed (ncu: +8 % time at 32768^2).
+#ifndef GD_STENCIL_CHECK_MASKED
+#define GD_STENCIL_CHECK_MASKED 1
+#endif
+    // (16-row strips, the HBM-size grids; at the L2-resident size's 8-row
+    // strips the predicated form measured faster: +17 % vs +29 % per access)
+    constexpr bool kCheckMasked = BIG && MODE == kCheck && ROWS >= 16 && GD_STENCIL_CHECK_MASKED;
     const uint32_t lane = threadIdx.x & 31u;
 #ifndef GD_STENCIL_FULL_WARP
 #define GD_STENCIL_FULL_WARP 1
@@ -99,37 +116,43 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         } else if constexpr (counts(MODE)) {
             const bool ok = BIG ? f16.in_big(pv) : (pv - f16.base) <= f16.lim;   // pv is 16-aligned (API)
             if (!ok) refm |= 1u << b;
-            if constexpr (MODE == kCheck || MODE == kClamp) {
+            if constexpr (kCheckMasked) {
+                v = __ldg(reinterpret_cast<const float4 *>(f16.addr_big(pv)));
+            } else if constexpr (MODE == kCheck || MODE == kClamp) {
                 // predicated: the destination is zeroed before the load (clamp:
-                // an outside vector is fixed up after its batch of loads, clampfix)
+                // an outside vector is fixed up after its batch of loads, clampfix).
+                // (Reading a refused vector from the trusted zero block instead,
+                // Fence::ld_at, measured 25 % slower per access at 32768^2.)
                 if (ok) v = __ldg(reinterpret_cast<const float4 *>(pv));
             } else {
-                v = __ldg(reinterpret_cast<const float4 *>(f16.addr(pv)));
+                v = __ldg(reinterpret_cast<const float4 *>(fa16(pv)));
             }
         } else {
-            v = __ldg(reinterpret_cast<const float4 *>(f16.addr(pv)));
+            v = __ldg(reinterpret_cast<const float4 *>(fa16(pv)));
         }
         return v;
     };
-    uint32_t hrefm = 0;                                // clamp: bit x of a halo word of row r0 + x outside
+    uint32_t hrefm = 0;                                // clamp / kCheckMasked: bit x of a halo word of row r0 + x outside
     auto ldh = [&](int hb) {                           // an edge lane's halo word of row r0 + hb, at ph (pv: the row below)
         float v = 0.f;
         if constexpr (MODE == kModulo && WALK) {
             if (need_h) v = __ldg(reinterpret_cast<const float *>(f4.step_down(fv, pv - ph)));
         } else if constexpr (counts(MODE)) {
-            const uint64_t fh = f4.addr(ph);
+            const uint64_t fh = fa4(ph);
             const bool ok = MODE == kMaskCount ? fh == ph : BIG ? f4.in_big(ph) : (ph - f4.base) <= f4.lim;
             if (need_h && !ok) nv++;
-            if constexpr (MODE == kClamp) {
+            if constexpr (MODE == kClamp || kCheckMasked) {
                 if (need_h && !ok) hrefm |= 1u << hb;
             }
-            if constexpr (MODE == kCheck || MODE == kClamp) {
+            if constexpr (kCheckMasked) {
+                if (need_h) v = __ldg(reinterpret_cast<const float *>(f4.addr_big(ph)));
+            } else if constexpr (MODE == kCheck || MODE == kClamp) {
                 if (need_h && ok) v = __ldg(reinterpret_cast<const float *>(ph));
             } else {
                 if (need_h) v = __ldg(reinterpret_cast<const float *>(fh));
             }
         } else {
-            if (need_h) v = __ldg(reinterpret_cast<const float *>(f4.addr(ph)));
+            if (need_h) v = __ldg(reinterpret_cast<const float *>(fa4(ph)));
         }
         return v;
     };
@@ -153,7 +176,7 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
             const uint4 val = make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
                                          __float_as_uint(o[3]));
             if constexpr (MODE == kMaskCount) {
-                const uint64_t f = f16.addr(po);
+                const uint64_t f = fa16(po);
                 nv += f != po ? 4u : 0u;                // inside iff the fence is the identity
                 st_v(f, val);
             } else if constexpr (MODE == kClamp) {     // (fence.cuh vst4, po 16-aligned)
@@ -166,7 +189,7 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
             } else {
                 const bool ok = BIG ? f16.in_big(po) : (po - f16.base) <= f16.lim;    // po is 16-aligned
                 if (counts(MODE) && !ok) nv += 4;
-                if (MODE != kCheck || ok) st_v(f16.addr(po), val);
+                if (MODE != kCheck || ok) st_v(fa16(po), val);
             }
         } else if (active) {                           // the grid's first / last columns
 #pragma unroll
@@ -185,6 +208,10 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         if (refm & 1u) P = clampfix(pv - 2 * step);
         if (refm & 2u) Cv = clampfix(pv - step);
     }
+    if constexpr (kCheckMasked) {
+        if (refm & 1u) P = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (refm & 2u) Cv = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
 #pragma unroll
     for (int i = 0; i < ROWS; i += kG) {
         if (!FULL && r0 + i >= r1) break;              // uniform over the CTA
@@ -199,6 +226,16 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
                 hv[g] = ldh(i + g);
                 pv += step;
                 ph += step;
+            }
+        }
+        if constexpr (kCheckMasked) {                  // rare: refused loads of this batch read 0
+            const uint32_t rows = (1u << kG) - 1u;
+            if (((refm >> (i + 2)) & rows) | ((hrefm >> i) & rows)) {
+#pragma unroll
+                for (int g = 0; g < kG; g++) {
+                    if (refm & (1u << (i + g + 2))) S[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (hrefm & (1u << (i + g))) hv[g] = 0.f;
+                }
             }
         }
         if constexpr (MODE == kClamp) {                // rare: outside accesses of this batch, after its loads
@@ -272,7 +309,7 @@ __device__ __forceinline__ void strip_rows(const FenceDesc &fd, uint64_t out, ui
                                            uint64_t pitch, float c0, float c1, uint64_t c, uint32_t r0, uint32_t r1,
                                            uint32_t &nv) {
     if (r1 - r0 == ROWS && (!GD_STENCIL_FULL_WARP || __all_sync(0xffffffffu, c >= 1 && c + 5 <= W))) {
-        if (counts(MODE) && MODE != kMaskCount && (fd.flags & kBig))
+        if (((counts(MODE) && MODE != kMaskCount) || MODE == kMask) && (fd.flags & kBig))
             strip<MODE, kG, ROWS, true, WALK, true>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
         else
             strip<MODE, kG, ROWS, true, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);

@@ -60,8 +60,9 @@ def time_modes(launch, reps, warm=3, extra=None):
         for m in res:
             for _ in range(warm):
                 go(m)
-        for _ in range(reps):
-            for m in res:
+        order = list(res)
+        for r in range(reps):
+            for m in order[r % len(order):] + order[:r % len(order)]:     # rotated: every position once
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(s)
                 go(m)
@@ -93,8 +94,9 @@ def time_modes_batched(launch, reps, batch=50, warm=3):
             graphs[m] = gr
         for m in res:
             graphs[m].replay()
-        for _ in range(reps):
-            for m in res:
+        order = list(res)
+        for r in range(reps):
+            for m in order[r % len(order):] + order[:r % len(order)]:     # rotated: every position once
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(s)
                 graphs[m].replay()
