@@ -116,7 +116,7 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "sm_min_mhz": min(sm) if sm else None, "reasons": reasons, "samples": len(self.rows)}
 
 
 # ---------------------------------------------------------------------------
@@ -696,12 +696,24 @@ def run_gpu(args):
     # ---- every kernel x every mode at the BASELINE sizes,
     #      hoisted (default) and per access; the L2-resident regime ----
     table = table_pa = l2 = l2_pa = None
+    tables_clocks = {}
     if not args.no_c5:
         w.rows_setup()
-        table = reduce_table(w.kernel_table(reps=args.table_reps), world, ALL_MODES)
-        table_pa = reduce_table(w.kernel_table(reps=args.table_reps, per_access=True), world, ALL_MODES)
-        l2 = reduce_table(w.l2_table(reps=args.table_reps), world, ALL_MODES)
-        l2_pa = reduce_table(w.l2_table(reps=args.table_reps, per_access=True), world, ALL_MODES)
+        # the SM clock during each table (nvidia-smi, 50 ms samples): late in a
+        # long run the power cap lowers it, which slows the ALU-heavier
+        # per-access variants more than their memory-bound twins
+        with Clocks(local) as ck:
+            table = reduce_table(w.kernel_table(reps=args.table_reps), world, ALL_MODES)
+        tables_clocks["kernels_all_modes"] = ck.summary()
+        with Clocks(local) as ck:
+            table_pa = reduce_table(w.kernel_table(reps=args.table_reps, per_access=True), world, ALL_MODES)
+        tables_clocks["kernels_all_modes_per_access"] = ck.summary()
+        with Clocks(local) as ck:
+            l2 = reduce_table(w.l2_table(reps=args.table_reps), world, ALL_MODES)
+        tables_clocks["l2_resident"] = ck.summary()
+        with Clocks(local) as ck:
+            l2_pa = reduce_table(w.l2_table(reps=args.table_reps, per_access=True), world, ALL_MODES)
+        tables_clocks["l2_resident_per_access"] = ck.summary()
 
     # ---- parity of the timed steps (cpu_baseline leg: the oracle on the host
     #      re-computes the sampled outputs; every rank checks its tenants) ----
@@ -739,6 +751,7 @@ def run_gpu(args):
             "kernels_all_modes_per_access": table_pa,
             "l2_resident": l2,
             "l2_resident_per_access": l2_pa,
+            "tables_clocks": tables_clocks,
             "cpu_baseline": cpu,
         }
         emit(line)

@@ -507,6 +507,27 @@ extern "C" gd_status gd_partition_fill(gd_arena *a, uint32_t id, uint32_t patter
 
 namespace gd {
 
+// Every byte an affine kernel may touch lies in [base, base + size)
+// (conservative extents: a false "no" only leaves the hoisting to the kernel).
+bool footprint_inside(const gd_work &w, uint64_t base, uint64_t size) {
+    uint64_t n = 0;
+    switch (w.kind) {
+        case GD_KIND_COPY:
+            return range_ok(base, size, w.ptr[0], w.u64[0]) && range_ok(base, size, w.ptr[1], w.u64[0]);
+        case GD_KIND_SAXPY:
+            return mul_ok(w.u64[0], 4, &n) && range_ok(base, size, w.ptr[0], n) && range_ok(base, size, w.ptr[1], n);
+        case GD_KIND_STENCIL: {
+            if (w.u32[2] != 0) return false;           // K5 v2: fenced through its tensor maps
+            const uint64_t H = w.u32[0], W = w.u32[1], pitch = w.u64[0];
+            uint64_t rows = 0;
+            if (!mul_ok(H, pitch, &rows) || !mul_ok(rows + W, 4, &n)) return false;
+            return range_ok(base, size, w.ptr[0], n) && range_ok(base, size, w.ptr[1], n);
+        }
+        default:
+            return false;                              // random accesses are fenced one by one
+    }
+}
+
 // Validate `w` (dry) or validate and launch it.  Structural errors are
 // returned before anything is issued.
 gd_status run_work_locked(gd_arena *a, const gd_work &w_in, cudaStream_t stream, bool dry, bool account,
@@ -593,6 +614,15 @@ gd_status run_work_locked(gd_arena *a, const gd_work &w_in, cudaStream_t stream,
     // scrubs, so the unfenced kernel cannot reach the new partition)
     const bool solo = w.mode != GD_MODE_NONE && solo_native(a);
     if (solo) w.mode = GD_MODE_NONE;
+    // R-hoist at launch granularity: an affine kernel (copy, saxpy, stencil
+    // v1) whose whole footprint lies in the partition performs exactly the
+    // accesses the check predicate allows, counts none, and every modulo /
+    // clamp fence of it is the identity, so the unfenced twin computes the same
+    // result; the host decides it from this launch's bounds snapshot (held
+    // stable by the launch guard until the enqueue).  The kernels' own
+    // per-CTA test still hoists the inner tiles of a launch that crosses the
+    // partition edge.  Mask mode is never hoisted, per-access launches never.
+    if (!per_access && hoistable(w.mode) && footprint_inside(w, base, size)) w.mode = GD_MODE_NONE;
 
     FenceDesc fd;
     fd.base = base;

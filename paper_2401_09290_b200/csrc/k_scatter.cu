@@ -15,10 +15,13 @@
 //   A1  k_scatter_part<M, 0>  every index: its fenced address -> slice id;
 //                             per-CTA shared histogram, one global atomic
 //                             per non-empty slice
-//   A2  k_scatter_scan        exclusive scan of the slice counts (one CTA)
+//   A2  k_scatter_scan        exclusive scan of the dense slices' counts
+//                             (one CTA)
 //   A3  k_scatter_part<M, 1>  the same fence again, refusals counted (once,
-//                             here), each update placed as (word offset,
-//                             value) in its slice's run of the scratch
+//                             here), each update of a dense slice placed as
+//                             (word offset, value) in its slice's run of the
+//                             scratch; an update of a sparse slice (fewer
+//                             updates than 128-byte lines) applied directly
 //   B   k_scatter_apply       the runs in slice order: RED.ADD.U32 at
 //                             base + 4 * word (CTAs in flight cover about one
 //                             slice, so its lines stay in L2)
@@ -47,6 +50,13 @@ constexpr int kU = 4;                                  // 16-byte index vectors 
 constexpr uint64_t kChunk = (uint64_t)kThreads * kU;   // vectors (4 indices each) per CTA
 constexpr int kSliceShift = 25;                        // 32 MiB slices
 constexpr uint32_t kMaxSlices = 512;                   // partitions up to 16 GiB (u32 word offsets)
+// A slice is dense when it holds on average an update per 128-byte line or
+// more: only dense slices are bucketed (and their lines streamed into L2 by
+// k_scatter_apply); the updates of a sparse slice (e.g. the wrapped
+// out-of-bounds updates of mask mode, spread thinly over the whole
+// partition) are applied directly in A3, where their random RMWs overlap
+// the pass's streaming, as the native twin's out-of-partition updates do.
+constexpr uint32_t kDense = (1u << kSliceShift) / 128;
 
 __device__ __forceinline__ uint4 ld_u4(uint64_t a) { return __ldcs(reinterpret_cast<const uint4 *>(a)); }
 __device__ __forceinline__ uint32_t ld_w(uint64_t a) { return __ldcs(reinterpret_cast<const unsigned int *>(a)); }
@@ -119,22 +129,47 @@ constexpr int kItems = 4 * kU;
 
 template <int SMODE, int MODE, int PASS>
 __device__ __forceinline__ void items(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src, uint64_t v0,
-                                      uint64_t nvec, uint32_t &nv, EdgeAcc &es, unsigned *hist,
+                                      uint64_t nvec, uint32_t &nv, EdgeAcc &es, unsigned *hist, const uint8_t *sparse,
                                       uint32_t (&w)[kItems], uint32_t (&rk)[kItems], uint32_t (&sv)[kItems],
                                       uint32_t &putm) {
     const Fence<SMODE, 16> f16(fd);
     const Fence<MODE, 4> f4(fd);
     uint4 j[kU], s[kU];
+    if constexpr (SMODE == kModulo) {
+        // per access: a thread's kU vectors of a stream lie kStep bytes
+        // apart; unless the stream straddles the base, each fenced address
+        // follows from the previous one (Fence::step_up, exactly the modulo)
+        constexpr uint64_t kStep = 16ull * kThreads;
+        const auto walk_ok = [&](uint64_t lo) {
+            const uint64_t hi = lo + kStep * (kU - 1) + 16;
+            return kStep < fd.size && lo <= hi && (hi <= fd.base || lo >= fd.base);
+        };
+        const bool wi = walk_ok(idx + 16 * v0), ws = walk_ok(src + 16 * v0);
+        uint64_t fi = 0, fs = 0;
 #pragma unroll
-    for (int u = 0; u < kU; u++) {
-        const uint64_t v = v0 + u * kThreads;
-        j[u] = make_uint4(0, 0, 0, 0);
-        s[u] = make_uint4(0, 0, 0, 0);
-        if (v < nvec) {
-            uint32_t c = 0;
-            j[u] = vld4(f16, idx + 16 * v, c, ld_u4, ld_w);
-            if (PASS == 1) s[u] = vld4(f16, src + 16 * v, c, ld_u4, ld_w);
-            if (PASS == 1) nv += c;
+        for (int u = 0; u < kU; u++) {
+            const uint64_t v = v0 + u * kThreads;
+            fi = (u == 0 || !wi) ? f16.addr(idx + 16 * v) : f16.step_up(fi, kStep);
+            if (PASS == 1) fs = (u == 0 || !ws) ? f16.addr(src + 16 * v) : f16.step_up(fs, kStep);
+            j[u] = make_uint4(0, 0, 0, 0);
+            s[u] = make_uint4(0, 0, 0, 0);
+            if (v < nvec) {
+                j[u] = ld_u4(fi);
+                if (PASS == 1) s[u] = ld_u4(fs);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const uint64_t v = v0 + u * kThreads;
+            j[u] = make_uint4(0, 0, 0, 0);
+            s[u] = make_uint4(0, 0, 0, 0);
+            if (v < nvec) {
+                uint32_t c = 0;
+                j[u] = vld4(f16, idx + 16 * v, c, ld_u4, ld_w);
+                if (PASS == 1) s[u] = vld4(f16, src + 16 * v, c, ld_u4, ld_w);
+                if (PASS == 1) nv += c;
+            }
         }
     }
     putm = 0;
@@ -146,7 +181,12 @@ __device__ __forceinline__ void items(const FenceDesc &fd, uint64_t table, uint6
         for (int q = 0; q < 4; q++) {
             const int k = 4 * u + q;
             uint64_t word = 0;
-            const bool put = live && resolve<MODE, PASS>(f4, table, (int32_t)jj[q], ss[q], nv, es, word);
+            bool put = live && resolve<MODE, PASS>(f4, table, (int32_t)jj[q], ss[q], nv, es, word);
+            if (PASS == 1 && put && sparse[word >> (kSliceShift - 2)]) {
+                // a sparse slice: applied here, at the fenced address (base + 4 word)
+                atomicAdd(reinterpret_cast<unsigned int *>(fd.base + 4 * word), ss[q]);
+                put = false;
+            }
             w[k] = (uint32_t)word;
             sv[k] = ss[q];
             rk[k] = put ? atomicAdd(&hist[w[k] >> (kSliceShift - 2)], 1u) : 0u;
@@ -162,7 +202,11 @@ __global__ void __launch_bounds__(kThreads) k_scatter_part(const __grid_constant
                                                            const unsigned *lim, uint2 *pairs) {
     __shared__ unsigned hist[kMaxSlices];
     __shared__ unsigned gpos[kMaxSlices];
-    for (uint32_t i = threadIdx.x; i < nslices; i += kThreads) hist[i] = 0;
+    __shared__ uint8_t sparse[kMaxSlices];             // A3: the slice's updates are applied directly
+    for (uint32_t i = threadIdx.x; i < nslices; i += kThreads) {
+        hist[i] = 0;
+        sparse[i] = PASS == 1 && cnt[i] < kDense;
+    }
     __syncthreads();
     uint32_t nv = 0, putm = 0;
     uint32_t w[kItems], rk[kItems], sv[kItems];
@@ -171,11 +215,11 @@ __global__ void __launch_bounds__(kThreads) k_scatter_part(const __grid_constant
     if constexpr (hoistable(MODE)) {                   // streams hoisted per CTA tile; RMWs fenced one by one
         const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
         if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, src + 16 * c0, 16 * cn))
-            items<kNone, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
+            items<kNone, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, sparse, w, rk, sv, putm);
         else
-            items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
+            items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, sparse, w, rk, sv, putm);
     } else {
-        items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
+        items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, sparse, w, rk, sv, putm);
     }
     __syncthreads();
     if constexpr (PASS == 0) {
@@ -230,7 +274,7 @@ __global__ void __launch_bounds__(kMaxSlices) k_scatter_scan(const unsigned *cnt
                                                              unsigned *total, uint32_t nslices) {
     __shared__ unsigned sh[kMaxSlices];
     const uint32_t t = threadIdx.x;
-    const unsigned c = t < nslices ? cnt[t] : 0u;
+    const unsigned c = t < nslices && cnt[t] >= kDense ? cnt[t] : 0u;   // sparse slices: no run (applied in A3)
     sh[t] = c;
     __syncthreads();
     for (uint32_t o = 1; o < kMaxSlices; o <<= 1) {  // inclusive Hillis-Steele scan
@@ -273,10 +317,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter_apply(uint64_t base, uint6
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + a), "r"((uint32_t)(b - a))
                              : "memory");
         };
-        // only dense slices (on average an update per 128-byte line or
-        // more) are worth streaming in whole; sparse ones are left to their
-        // REDs' own sector fills
-        constexpr uint32_t kDense = (1u << kSliceShift) / 128;
+        // (every bucketed slice is dense: sparse ones were applied in A3)
         if (st == 0 && c >= kDense) prefetch(s, st);                     // the first slice: its own lines
         if (e < n) {
             const uint32_t s2 = pairs[e].x >> (kSliceShift - 2);         // the next updated slice

@@ -47,8 +47,17 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
     const Fence<MODE, 4> f4(fd);
     // the mask fence of a 16- / 4-aligned address (BIG: one LOP3, Fence::addr_big)
     constexpr bool kMaskBig = BIG && (MODE == kMask || MODE == kMaskCount);
-    auto fa16 = [&](uint64_t a) { return kMaskBig ? f16.addr_big(a) : f16.addr(a); };
-    auto fa4 = [&](uint64_t a) { return kMaskBig ? f4.addr_big(a) : f4.addr(a); };
+    // MASK on a kBig partition walks fenced pointers: F(F(a) + s) = F(a + s)
+    // for the mask fence (the low words and the carry out of them are the
+    // same, and base's bits lie above the mask's), so a row's fenced address
+    // is the previous row's plus the row step, fenced in place (adv: one LOP3
+    // and no copy of the unfenced pointer); fa16 / fa4 are then the identity
+#ifndef GD_STENCIL_MASK_WALK
+#define GD_STENCIL_MASK_WALK 1
+#endif
+    constexpr bool kMaskWalk = BIG && MODE == kMask && GD_STENCIL_MASK_WALK;
+    auto fa16 = [&](uint64_t a) { return kMaskWalk ? a : kMaskBig ? f16.addr_big(a) : f16.addr(a); };
+    auto fa4 = [&](uint64_t a) { return kMaskWalk ? a : kMaskBig ? f4.addr_big(a) : f4.addr(a); };
     // CHECK on a kBig partition: every load is issued, unpredicated, at its
     // mask-fenced address (inside the tenant's own partition), and a refused
     // load's value is replaced by 0 after its batch of loads (zerofix below,
@@ -96,6 +105,15 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
     uint64_t pv = in + 4 * ((uint64_t)(r0 - 1) * pitch + cl);                 // vector of row r0 - 1
     uint64_t ph = in + 4 * ((uint64_t)r0 * pitch + (lane == 0 ? c - 1 : c + 4));   // halo word of row r0
     uint64_t po = out + 4 * ((uint64_t)r0 * pitch + c);                       // output vector of row r0
+    if constexpr (kMaskWalk) {
+        pv = f16.addr_big(pv);
+        ph = f16.addr_big(ph);
+        po = f16.addr_big(po);
+    }
+    auto adv = [&](uint64_t &p) {                      // the pointer of the next row
+        p += step;
+        if constexpr (kMaskWalk) p = f16.addr_big(p);
+    };
     // counting modes: bit b of refm = the vector of row r0 - 1 + b lies
     // outside the partition (one predicated OR per load, the bit a
     // compile-time constant); its refused logical accesses are weighted
@@ -201,9 +219,9 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
         }
     };
     float4 P = ldv(0);
-    pv += step;
+    adv(pv);
     float4 Cv = ldv(1);
-    pv += step;
+    adv(pv);
     if constexpr (MODE == kClamp) {
         if (refm & 1u) P = clampfix(pv - 2 * step);
         if (refm & 2u) Cv = clampfix(pv - step);
@@ -224,8 +242,8 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
             if (FULL || r0 + i + g < r1) {
                 S[g] = ldv(i + g + 2);
                 hv[g] = ldh(i + g);
-                pv += step;
-                ph += step;
+                adv(pv);
+                adv(ph);
             }
         }
         if constexpr (kCheckMasked) {                  // rare: refused loads of this batch read 0
@@ -275,7 +293,7 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
                     o[k] = __fmaf_rn(c1, s, __fmul_rn(c0, cc[k]));
                 }
                 stv(i + g, o);
-                po += step;
+                adv(po);
             }
         }
         // slide the window: rows r+kG-1 (new P) and r+kG (new C)

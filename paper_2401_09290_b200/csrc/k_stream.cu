@@ -26,6 +26,18 @@ __device__ __forceinline__ void st16(uint64_t a, uint4 v) { __stcs(reinterpret_c
 __device__ __forceinline__ uint32_t ld4(uint64_t a) { return __ldcs(reinterpret_cast<const unsigned int *>(a)); }
 __device__ __forceinline__ void st4(uint64_t a, uint32_t v) { __stcs(reinterpret_cast<unsigned int *>(a), v); }
 
+// MODULO per access (hoisting off, or a CTA touching the partition edge): a
+// thread's kU vectors of one stream lie kStep bytes apart, so when the
+// stream's range does not straddle the base (its u64 offsets from the base do
+// not wrap, reading A10) and kStep < size, each fenced address follows from
+// the previous one (Fence::step_up: one add, one compare, one select),
+// exactly the full modulo; otherwise every access takes the full modulo.
+constexpr uint64_t kStep = 16ull * kThreads;
+__device__ __forceinline__ bool walk_ok(const FenceDesc &fd, uint64_t lo) {
+    const uint64_t hi = lo + kStep * (kU - 1) + 16;
+    return kStep < fd.size && lo <= hi && (hi <= fd.base || lo >= fd.base);
+}
+
 // ---------------------------------------------------------------------------
 // K1: dst[0:n) = src[0:n).  Logical accesses (oracle or_copy): per 16-byte
 // unit one load + one store; per tail byte one load + one store.
@@ -35,6 +47,24 @@ __device__ __forceinline__ void copy_chunk(const FenceDesc &fd, uint64_t dst, ui
                                            uint64_t nvec, uint32_t &nv) {
     const Fence<MODE, 16> f(fd);
     uint4 r[kU];
+    if constexpr (MODE == kModulo) {
+        const bool ws = walk_ok(fd, src + 16 * v0), wd = walk_ok(fd, dst + 16 * v0);
+        uint64_t fa = 0;
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const uint64_t v = v0 + u * kThreads, a = src + 16 * v;
+            fa = (u == 0 || !ws) ? f.addr(a) : f.step_up(fa, kStep);
+            r[u] = make_uint4(0, 0, 0, 0);
+            if (v < nvec) r[u] = ld16(fa);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const uint64_t v = v0 + u * kThreads, a = dst + 16 * v;
+            fa = (u == 0 || !wd) ? f.addr(a) : f.step_up(fa, kStep);
+            if (v < nvec) st16(fa, r[u]);
+        }
+        return;
+    }
 #pragma unroll
     for (int u = 0; u < kU; u++) {
         const uint64_t v = v0 + u * kThreads;
@@ -90,6 +120,34 @@ __device__ __forceinline__ void saxpy_chunk(const FenceDesc &fd, float alpha, ui
                                             uint64_t nvec, uint32_t &nv) {
     const Fence<MODE, 16> f(fd);
     uint4 xv[kU], yv[kU];
+    if constexpr (MODE == kModulo) {
+        const bool wx = walk_ok(fd, x + 16 * v0), wy = walk_ok(fd, y + 16 * v0);
+        uint64_t fx = 0, fy = 0;
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const uint64_t v = v0 + u * kThreads;
+            fx = (u == 0 || !wx) ? f.addr(x + 16 * v) : f.step_up(fx, kStep);
+            fy = (u == 0 || !wy) ? f.addr(y + 16 * v) : f.step_up(fy, kStep);
+            xv[u] = make_uint4(0, 0, 0, 0);
+            yv[u] = xv[u];
+            if (v < nvec) {
+                xv[u] = ld16(fx);
+                yv[u] = ld16(fy);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++) {      // the y walk again for the stores (fewer live registers)
+            const uint64_t v = v0 + u * kThreads;
+            fy = (u == 0 || !wy) ? f.addr(y + 16 * v) : f.step_up(fy, kStep);
+            if (v < nvec)
+                st16(fy, make_uint4(
+                    __float_as_uint(__fmaf_rn(alpha, __uint_as_float(xv[u].x), __uint_as_float(yv[u].x))),
+                    __float_as_uint(__fmaf_rn(alpha, __uint_as_float(xv[u].y), __uint_as_float(yv[u].y))),
+                    __float_as_uint(__fmaf_rn(alpha, __uint_as_float(xv[u].z), __uint_as_float(yv[u].z))),
+                    __float_as_uint(__fmaf_rn(alpha, __uint_as_float(xv[u].w), __uint_as_float(yv[u].w)))));
+        }
+        return;
+    }
 #pragma unroll
     for (int u = 0; u < kU; u++) {
         const uint64_t v = v0 + u * kThreads;

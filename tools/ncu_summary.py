@@ -15,6 +15,7 @@ import sys
 METRICS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram__cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__bytes.sum.per_second",
     "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread", "launch__grid_size",
     "launch__block_size", "launch__occupancy_limit_registers", "sm__warps_active.avg.pct_of_peak_sustained_active",
@@ -76,8 +77,14 @@ def main():
                 key = (f"{mm.group(1)}<{mm.group(2).replace(' ', '')}>" if mm
                        else re.sub(r"^.*::", "", re.sub(r"\(.*", "", name)))
                 traffic[key] = rd + wr
-                if "dram__throughput.avg.pct_of_peak_sustained_elapsed" in d:
-                    traffic[key + ":dram_pct"] = d["dram__throughput.avg.pct_of_peak_sustained_elapsed"]["value"]
+                # ncu's DRAM throughput, % of its theoretical peak (B200: 2048 B per
+                # DRAM cycle x 3.996 GHz = 8.18 TB/s); this ncu reports it as
+                # gpu__dram_throughput (dram__throughput reads "-")
+                for pm in ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+                           "dram__throughput.avg.pct_of_peak_sustained_elapsed"):
+                    if pm in d:
+                        traffic[key + ":dram_pct"] = d[pm]["value"]
+                        break
                 traffic["_source"] = f"ncu --set full, {os.path.basename(rep)}"
                 print(f"   traffic (dram read+write) = {rd + wr:.4e} B")
     if out:
