@@ -15,13 +15,10 @@
 //   A1  k_scatter_part<M, 0>  every index: its fenced address -> slice id;
 //                             per-CTA shared histogram, one global atomic
 //                             per non-empty slice
-//   A2  k_scatter_scan        exclusive scan of the dense slices' counts
-//                             (one CTA)
+//   A2  k_scatter_scan        exclusive scan of the slice counts (one CTA)
 //   A3  k_scatter_part<M, 1>  the same fence again, refusals counted (once,
-//                             here), each update of a dense slice placed as
-//                             (word offset, value) in its slice's run of the
-//                             scratch; an update of a sparse slice (fewer
-//                             updates than 128-byte lines) applied directly
+//                             here), each update placed as (word offset,
+//                             value) in its slice's run of the scratch
 //   B   k_scatter_apply       the runs in slice order: RED.ADD.U32 at
 //                             base + 4 * word (CTAs in flight cover about one
 //                             slice, so its lines stay in L2)
@@ -50,13 +47,6 @@ constexpr int kU = 4;                                  // 16-byte index vectors 
 constexpr uint64_t kChunk = (uint64_t)kThreads * kU;   // vectors (4 indices each) per CTA
 constexpr int kSliceShift = 25;                        // 32 MiB slices
 constexpr uint32_t kMaxSlices = 512;                   // partitions up to 16 GiB (u32 word offsets)
-// A slice is dense when it holds on average an update per 128-byte line or
-// more: only dense slices are bucketed (and their lines streamed into L2 by
-// k_scatter_apply); the updates of a sparse slice (e.g. the wrapped
-// out-of-bounds updates of mask mode, spread thinly over the whole
-// partition) are applied directly in A3, where their random RMWs overlap
-// the pass's streaming, as the native twin's out-of-partition updates do.
-constexpr uint32_t kDense = (1u << kSliceShift) / 128;
 
 __device__ __forceinline__ uint4 ld_u4(uint64_t a) { return __ldcs(reinterpret_cast<const uint4 *>(a)); }
 __device__ __forceinline__ uint32_t ld_w(uint64_t a) { return __ldcs(reinterpret_cast<const unsigned int *>(a)); }
@@ -129,46 +119,63 @@ constexpr int kItems = 4 * kU;
 
 template <int SMODE, int MODE, int PASS>
 __device__ __forceinline__ void items(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src, uint64_t v0,
-                                      uint64_t nvec, uint32_t &nv, EdgeAcc &es, unsigned *hist, const uint8_t *sparse,
+                                      uint64_t nvec, uint32_t &nv, EdgeAcc &es, unsigned *hist,
                                       uint32_t (&w)[kItems], uint32_t (&rk)[kItems], uint32_t (&sv)[kItems],
                                       uint32_t &putm) {
     const Fence<SMODE, 16> f16(fd);
     const Fence<MODE, 4> f4(fd);
     uint4 j[kU], s[kU];
-    if constexpr (SMODE == kModulo) {
-        // per access: a thread's kU vectors of a stream lie kStep bytes
-        // apart; unless the stream straddles the base, each fenced address
-        // follows from the previous one (Fence::step_up, exactly the modulo)
-        constexpr uint64_t kStep = 16ull * kThreads;
-        const auto walk_ok = [&](uint64_t lo) {
-            const uint64_t hi = lo + kStep * (kU - 1) + 16;
-            return kStep < fd.size && lo <= hi && (hi <= fd.base || lo >= fd.base);
-        };
-        const bool wi = walk_ok(idx + 16 * v0), ws = walk_ok(src + 16 * v0);
-        uint64_t fi = 0, fs = 0;
+    // Every load of the 2 kU is issued unconditionally, with no branch
+    // between them (a branch per vector had made ptxas consume each loaded
+    // index vector before issuing the next load: four serial DRAM round
+    // trips, ncu: +26 % time for the mask pass A3): a dead vector (past
+    // nvec) or a refused one (check) reads the trusted zero block, so it
+    // reads 0 as a refused check-mode load must (reading A1); under clamp
+    // an outside vector is then replaced by its edge word four times
+    // (fence.cuh vld4), after every load has been issued.
+    // MODULO walks each stream: a thread's kU vectors of a stream lie
+    // kStep bytes apart, so unless the stream straddles the base each
+    // fenced address follows from the previous one (Fence::step_up,
+    // exactly the full modulo).
+    constexpr uint64_t kStep = 16ull * kThreads;
+    const auto walk_ok = [&](uint64_t lo) {
+        const uint64_t hi = lo + kStep * (kU - 1) + 16;
+        return SMODE == kModulo && kStep < fd.size && lo <= hi && (hi <= fd.base || lo >= fd.base);
+    };
+    const bool wi = walk_ok(idx + 16 * v0), ws = walk_ok(src + 16 * v0);
+    uint64_t fi = 0, fs = 0;
+    uint32_t outm = 0;                             // clamp: bit 2u / 2u+1 = idx / src vector u outside
 #pragma unroll
-        for (int u = 0; u < kU; u++) {
-            const uint64_t v = v0 + u * kThreads;
-            fi = (u == 0 || !wi) ? f16.addr(idx + 16 * v) : f16.step_up(fi, kStep);
-            if (PASS == 1) fs = (u == 0 || !ws) ? f16.addr(src + 16 * v) : f16.step_up(fs, kStep);
-            j[u] = make_uint4(0, 0, 0, 0);
-            s[u] = make_uint4(0, 0, 0, 0);
-            if (v < nvec) {
-                j[u] = ld_u4(fi);
-                if (PASS == 1) s[u] = ld_u4(fs);
-            }
+    for (int u = 0; u < kU; u++) {
+        const uint64_t v = v0 + u * kThreads, ai = idx + 16 * v, as = src + 16 * v;
+        const bool live = v < nvec;
+        fi = (u == 0 || !wi) ? f16.addr(ai) : f16.step_up(fi, kStep);
+        fs = (u == 0 || !ws) ? f16.addr(as) : f16.step_up(fs, kStep);
+        bool oki = true, oks = true;
+        if constexpr (counts(SMODE)) {             // the check predicate (16-aligned vectors)
+            oki = f16.ok_aligned_in(ai);
+            oks = f16.ok_aligned_in(as);
+            if (PASS == 1 && live) nv += (oki ? 0u : 4u) + (oks ? 0u : 4u);
         }
-    } else {
+        constexpr bool kRefuse = SMODE == kCheck || SMODE == kClamp;
+        if (SMODE == kClamp && live) outm |= (oki ? 0u : 1u << (2 * u)) | (oks ? 0u : 2u << (2 * u));
+        j[u] = ld_u4(live && (!kRefuse || oki) ? (SMODE == kClamp ? ai : fi) : fd.zero);
+        s[u] = make_uint4(0, 0, 0, 0);
+        if (PASS == 1) s[u] = ld_u4(live && (!kRefuse || oks) ? (SMODE == kClamp ? as : fs) : fd.zero);
+    }
+    if constexpr (SMODE == kClamp) {
+        if (outm) {                                // rare: outside vectors, edge word four times
 #pragma unroll
-        for (int u = 0; u < kU; u++) {
-            const uint64_t v = v0 + u * kThreads;
-            j[u] = make_uint4(0, 0, 0, 0);
-            s[u] = make_uint4(0, 0, 0, 0);
-            if (v < nvec) {
-                uint32_t c = 0;
-                j[u] = vld4(f16, idx + 16 * v, c, ld_u4, ld_w);
-                if (PASS == 1) s[u] = vld4(f16, src + 16 * v, c, ld_u4, ld_w);
-                if (PASS == 1) nv += c;
+            for (int u = 0; u < kU; u++) {
+                const uint64_t v = v0 + u * kThreads;
+                if (outm & (1u << (2 * u))) {
+                    const uint32_t x = ld_w(f16.edge4(idx + 16 * v));
+                    j[u] = make_uint4(x, x, x, x);
+                }
+                if (PASS == 1 && (outm & (2u << (2 * u)))) {
+                    const uint32_t x = ld_w(f16.edge4(src + 16 * v));
+                    s[u] = make_uint4(x, x, x, x);
+                }
             }
         }
     }
@@ -181,12 +188,7 @@ __device__ __forceinline__ void items(const FenceDesc &fd, uint64_t table, uint6
         for (int q = 0; q < 4; q++) {
             const int k = 4 * u + q;
             uint64_t word = 0;
-            bool put = live && resolve<MODE, PASS>(f4, table, (int32_t)jj[q], ss[q], nv, es, word);
-            if (PASS == 1 && put && sparse[word >> (kSliceShift - 2)]) {
-                // a sparse slice: applied here, at the fenced address (base + 4 word)
-                atomicAdd(reinterpret_cast<unsigned int *>(fd.base + 4 * word), ss[q]);
-                put = false;
-            }
+            const bool put = live && resolve<MODE, PASS>(f4, table, (int32_t)jj[q], ss[q], nv, es, word);
             w[k] = (uint32_t)word;
             sv[k] = ss[q];
             rk[k] = put ? atomicAdd(&hist[w[k] >> (kSliceShift - 2)], 1u) : 0u;
@@ -202,11 +204,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter_part(const __grid_constant
                                                            const unsigned *lim, uint2 *pairs) {
     __shared__ unsigned hist[kMaxSlices];
     __shared__ unsigned gpos[kMaxSlices];
-    __shared__ uint8_t sparse[kMaxSlices];             // A3: the slice's updates are applied directly
-    for (uint32_t i = threadIdx.x; i < nslices; i += kThreads) {
-        hist[i] = 0;
-        sparse[i] = PASS == 1 && cnt[i] < kDense;
-    }
+    for (uint32_t i = threadIdx.x; i < nslices; i += kThreads) hist[i] = 0;
     __syncthreads();
     uint32_t nv = 0, putm = 0;
     uint32_t w[kItems], rk[kItems], sv[kItems];
@@ -215,11 +213,11 @@ __global__ void __launch_bounds__(kThreads) k_scatter_part(const __grid_constant
     if constexpr (hoistable(MODE)) {                   // streams hoisted per CTA tile; RMWs fenced one by one
         const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
         if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, src + 16 * c0, 16 * cn))
-            items<kNone, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, sparse, w, rk, sv, putm);
+            items<kNone, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
         else
-            items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, sparse, w, rk, sv, putm);
+            items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
     } else {
-        items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, sparse, w, rk, sv, putm);
+        items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
     }
     __syncthreads();
     if constexpr (PASS == 0) {
@@ -274,7 +272,7 @@ __global__ void __launch_bounds__(kMaxSlices) k_scatter_scan(const unsigned *cnt
                                                              unsigned *total, uint32_t nslices) {
     __shared__ unsigned sh[kMaxSlices];
     const uint32_t t = threadIdx.x;
-    const unsigned c = t < nslices && cnt[t] >= kDense ? cnt[t] : 0u;   // sparse slices: no run (applied in A3)
+    const unsigned c = t < nslices ? cnt[t] : 0u;
     sh[t] = c;
     __syncthreads();
     for (uint32_t o = 1; o < kMaxSlices; o <<= 1) {  // inclusive Hillis-Steele scan
@@ -317,7 +315,10 @@ __global__ void __launch_bounds__(kThreads) k_scatter_apply(uint64_t base, uint6
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + a), "r"((uint32_t)(b - a))
                              : "memory");
         };
-        // (every bucketed slice is dense: sparse ones were applied in A3)
+        // only dense slices (on average an update per 128-byte line or
+        // more) are worth streaming in whole; sparse ones are left to their
+        // REDs' own sector fills
+        constexpr uint32_t kDense = (1u << kSliceShift) / 128;
         if (st == 0 && c >= kDense) prefetch(s, st);                     // the first slice: its own lines
         if (e < n) {
             const uint32_t s2 = pairs[e].x >> (kSliceShift - 2);         // the next updated slice

@@ -422,9 +422,13 @@ cudaError_t stencil_t(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t H
         if (pa) k_stencil_pa<MODE, kRows><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
         else k_stencil<MODE, kRows><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
     } else {
-        const dim3 grid((unsigned)gx, (unsigned)((H - 2ull + 7) / 8));
-        if (pa) k_stencil_pa<MODE, 8><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
-        else k_stencil<MODE, 8><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
+#ifndef GD_STENCIL_SMALL_ROWS
+#define GD_STENCIL_SMALL_ROWS 8
+#endif
+        constexpr int kSmall = GD_STENCIL_SMALL_ROWS;
+        const dim3 grid((unsigned)gx, (unsigned)((H - 2ull + kSmall - 1) / kSmall));
+        if (pa) k_stencil_pa<MODE, kSmall><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
+        else k_stencil<MODE, kSmall><<<grid, kThreads, 0, s>>>(fd, out, in, H, W, pitch, c0, c1);
     }
     return cudaGetLastError();
 }

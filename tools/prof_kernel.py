@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--D", type=int, default=32, help="row width (words) for --kind gatherrows")
     ap.add_argument("--pa", action="store_true", help="per-access fencing (GD_FENCE_PER_ACCESS)")
     ap.add_argument("--l2", action="store_true", help="stencil at the L2-resident size 2048^2")
+    ap.add_argument("--oob", type=float, default=0.01, help="gather / scatter: fraction of planted out-of-partition indices")
     a = ap.parse_args()
     if a.pa:
         a.mode += "+pa"
@@ -39,7 +40,7 @@ def main():
         # C3: uniform in-bounds indices into the 2^29-entry table, 1 % planted below the base
         idx = devmem.view(b + 2 * GiB, 1 << 26, torch.int32)
         idx.random_(0, 1 << 29, generator=gen)
-        pos = torch.randperm(1 << 26, generator=gen, device="cuda:0")[: (1 << 26) // 100]
+        pos = torch.randperm(1 << 26, generator=gen, device="cuda:0")[: int((1 << 26) * a.oob)]
         idx[pos] = torch.randint(-2**31, 0, (pos.numel(),), generator=gen, device="cuda:0", dtype=torch.int32)
         devmem.view(b, 1 << 29, torch.int32).random_(generator=gen)
     if a.kind == "gatherrows":
