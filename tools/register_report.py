@@ -22,6 +22,13 @@ def demangle(names):
     return dict(zip(names, out))
 
 
+def ctas_by_regs(regs, threads=256):
+    """CTAs of `threads` per SM the register file allows (64 K registers per
+    SM, allocated per warp in units of 256 registers)."""
+    per_warp = -(-regs * 32 // 256) * 256
+    return (65536 // per_warp) // (threads // 32)
+
+
 def main():
     rows = {}
     for log in sorted(glob.glob(os.path.join(BUILD, "ptxas_*.log"))):
@@ -48,7 +55,13 @@ def main():
         if "none" not in modes:
             continue
         base = modes["none"]["regs"]
-        report["kernels"][k] = {m: dict(v, delta_regs=v["regs"] - base) for m, v in modes.items()}
+        # every kernel here runs 256-thread CTAs; the occupancy that matters
+        # is the register-limited CTA count (each kernel's __launch_bounds__
+        # caps it anyway), so report it beside the raw register delta
+        occ0 = ctas_by_regs(base)
+        report["kernels"][k] = {m: dict(v, delta_regs=v["regs"] - base, ctas_per_sm_by_regs=ctas_by_regs(v["regs"]),
+                                        occupancy_change=ctas_by_regs(v["regs"]) - occ0)
+                                for m, v in modes.items()}
         for m, v in modes.items():
             if m != "none":
                 deltas.append(v["regs"] - base)
@@ -58,9 +71,13 @@ def main():
         hist[str(d)] = hist.get(str(d), 0) + 1
     report["delta_histogram"] = dict(sorted(hist.items(), key=lambda kv: int(kv[0])))
     report["all_zero_local_memory"] = all(v["stack"] == 0 for m in table.values() for v in m.values())
+    report["fenced_variants_with_lower_occupancy"] = sorted(
+        f"{k}/{m}" for k, ms in report["kernels"].items() for m, v in ms.items() if v["occupancy_change"] < 0)
     for k, modes in report["kernels"].items():
         print(f"{k:12s} " + "  ".join(f"{m}:{v['regs']}({v['delta_regs']:+d})" for m, v in modes.items()))
     print("delta histogram (fenced - unfenced registers):", report["delta_histogram"])
+    print("fenced variants with fewer register-limited CTAs per SM than their twin:",
+          report["fenced_variants_with_lower_occupancy"])
     if "--out" in sys.argv:
         json.dump(report, open(sys.argv[sys.argv.index("--out") + 1], "w"), indent=1)
 
