@@ -23,7 +23,7 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex
 echo "ncu rc=$?" >> $O/ncu_bench.out
 cap() {  # name, kernel regex, prof_kernel args...
   local n=$1 k=$2; shift 2
-  timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$k" -s 1 -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$k" -s 1 -c 1 \
       -o $O/prof_$n -f python tools/prof_kernel.py --reps 2 "$@" > $O/prof_$n.log 2>&1
   echo "$n rc=$?" >> $O/prof_$n.log
 }
