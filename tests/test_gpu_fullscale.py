@@ -229,6 +229,54 @@ def test_c4_stencil_full_out_crossing_end(arenas, mode):
             assert not got.any(), f"row {r}: a refused store landed"     # scrubbed, never written
 
 
+@pytest.mark.parametrize("mode", ["mask", "check", "modulo", "maskcount", "clamp"])
+def test_c4_stencil_full_in_crossing_end(arenas, mode):
+    """The input side of the C4 layout at the bench size: `in` at
+    end - (H-64)·pitch·4, so its rows H-64 .. H-1 lie wholly past the end
+    (16 GiB partition: the >= 4 GiB path of the stencil, incl. check mode's
+    masked loads with their zero fix-up when run per access by
+    test_gpu_peraccess.py).  Each point's five loads resolve per the mode:
+    mask / modulo / mask-count read the row wrapped to offset
+    (4·x·W + in - base) mod size (filled with random floats), check reads 0,
+    clamp reads the partition's last word (fence.cuh edge4); the counting
+    modes count (W-2)·(64 + 3·63 + 62) refused loads (N of rows >= H-63, C/W/E
+    of rows >= H-64, S of rows >= H-65).  Sampled rows against the oracle's
+    stencil over the 3-row band built that way."""
+    a = arenas(PART)
+    p = a.partition_alloc(PART)
+    H = W = 32768
+    inp, out = p.end - (H - 64) * W * 4, p.base + 4 * GiB
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(4002)
+    devmem.view(inp, (H - 64) * W, torch.float32).uniform_(0, 1, generator=gen)
+    devmem.view(p.base, 64 * W, torch.float32).uniform_(0, 1, generator=gen)     # the wrap target
+    torch.cuda.synchronize()
+    a.stats_reset()
+    a.stencil(p.id, mode, out, inp, H, W, W, 0.5, 0.125)
+    v = a.stats(p.id)["violations"]
+    assert v == ((W - 2) * (64 + 3 * 63 + 62) if mode in ("check", "maskcount", "clamp") else 0)
+    last = download(p.end - 4, 4)                                                # clamp's edge word
+
+    def in_row(x):
+        addr = inp + 4 * x * W
+        if addr + 4 * W <= p.end:
+            return download(addr, 4 * W)
+        if mode == "check":
+            return np.zeros(4 * W, np.uint8)
+        if mode == "clamp":
+            return np.tile(last, W)
+        return download(p.base + (addr - p.base) % p.size, 4 * W)               # mask = modulo (pow2)
+
+    for r in [1, 1000, H - 67, H - 66, H - 65, H - 64, H - 63, H - 3, H - 2]:
+        band = np.concatenate([in_row(x) for x in (r - 1, r, r + 1)])
+        m = oracle.Mem(0x20000000, 4 << 20)
+        m.buf[:band.size] = band
+        oracle.stencil(m, 0x20000000, 4 << 20, "none", 0x20000000 + (2 << 20), 0x20000000, 3, W, W, 0.5, 0.125)
+        want = m.view(0x20000000 + (2 << 20) + 4 * W, np.uint32, W)[1:W - 1]
+        got = download(out + 4 * r * W, 4 * W).view(np.uint32)[1:W - 1]
+        np.testing.assert_array_equal(got, want, err_msg=f"row {r}")
+
+
 def test_c4_stencil_v2_full_sampled_rows(arenas):
     """K5 v2 at the BASELINE size in the bench's launch configuration: sampled
     rows (incl. tile edges at 16-row and 248-column boundaries) against the

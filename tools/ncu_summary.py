@@ -61,6 +61,8 @@ def main():
     reps = [a for a in args if a.endswith(".ncu-rep")]
     summary = {}
     tpath = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
+    if "--traffic" in args:                            # e.g. on the GPU box: a copy under gpurun_out/
+        tpath = args[args.index("--traffic") + 1]
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for rep in reps:
         for d in read(rep):

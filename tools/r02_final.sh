@@ -7,13 +7,15 @@
 cd "$(dirname "$0")/.."
 O=gpurun_out/r02final; mkdir -p $O
 nvidia-smi --query-gpu=name,memory.total,clocks.max.sm,clocks.sm,power.limit --format=csv > $O/gpuinfo.txt 2>&1
+if [ -z "$SKIP_SUITES" ]; then
 timeout 1500 python -m pytest -q -p no:cacheprovider -m gpu tests --durations=15 > $O/pytest.log 2>&1
 echo "rc=$?" >> $O/pytest.log
 GD_CHECK_PER_ACCESS=1 timeout 1500 python -m pytest -q -p no:cacheprovider -m gpu tests --durations=5 > $O/pytest_pa.log 2>&1
 echo "rc=$?" >> $O/pytest_pa.log
+fi
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
 echo "smoke rc=$?" >> $O/smoke.log
-for i in 1 2 3; do
+for i in $(seq 1 ${BENCH_RUNS:-3}); do
   timeout 1200 python bench.py > $O/bench_$i.json 2> $O/bench_$i.err
   echo "bench rc=$?" >> $O/bench_$i.err
 done
@@ -42,7 +44,13 @@ for m in check modulo maskcount clamp; do
   cap stencilpa_$m k_stencil_pa --kind stencil --mode $m --pa
   cap gatherrowspa_$m k_gatherR --kind gatherrows --D 32 --mode $m --pa
 done
+# summarise on the box (gpurun brings back at most 64 MiB): every capture
+# into one JSON, DRAM bytes + throughput per kernel into a copy of
+# profiles/ncu_traffic.json; keep the .ncu-rep of the dominant kernel only
+cp profiles/ncu_traffic.json $O/ncu_traffic.json
+python tools/ncu_summary.py $O/prof_*.ncu-rep --out $O/ncu_full.json --traffic $O/ncu_traffic.json > $O/ncu_full.txt 2>&1
+for f in $O/prof_*.ncu-rep; do case $f in *prof_saxpy_mask.ncu-rep) ;; *) rm -f $f ;; esac; done
 M=none,mask,check,modulo,maskcount,clamp,check+pa,modulo+pa,maskcount+pa,clamp+pa
 timeout 1500 python tools/kernel_bench.py --reps 12 --only copy,saxpy,gather,scatter,gatherrows,stencil,stencil_tma,l2,gemm --modes $M > $O/kb.json 2> $O/kb.txt
 echo "kb rc=$?" >> $O/kb.txt
-tail -3 $O/pytest.log; tail -3 $O/pytest_pa.log; cat $O/smoke.log; for i in 1 2 3; do head -c 300 $O/bench_$i.json; echo; done; tail -2 $O/ncu_bench.out; grep -h "rc=" $O/prof_*.log | sort | uniq -c | sort -rn | head; tail -30 $O/kb.txt
+tail -3 $O/pytest.log; tail -3 $O/pytest_pa.log; cat $O/smoke.log; for f in $O/bench_*.json; do head -c 300 $f; echo; done; du -sh $O; tail -2 $O/ncu_bench.out; grep -h "rc=" $O/prof_*.log | sort | uniq -c | sort -rn | head; tail -30 $O/kb.txt
