@@ -38,6 +38,14 @@ MiB = 1 << 20
 ALL_MODES = ("none", "mask", "check", "modulo", "maskcount", "clamp")
 
 
+def gpu_config(mode, world):
+    """The bench line's config (both arms)."""
+    return {"workload": WORKLOAD, "mode": mode, "tenants_per_gpu": TENANTS,
+            "partition_bytes": PART, "copy_bytes": COPY_BYTES, "saxpy_n": SAXPY_N,
+            "l2": "inputs larger than L2 (4 GiB per tensor vs 126 MB L2), no flush",
+            "parallelism": f"{world} GPU(s), one arena per GPU, tenants sharded, no data-path collective"}
+
+
 def paper_mean(xs):
     """The paper's statistic: the mean without the minimum and
     the maximum (of its 10 runs; here of the table's repetitions)."""
@@ -744,10 +752,7 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (torch.Generator seeded 1000*2+tenant: random bytes, U[-1,1) fp32)",
-            "config": {"workload": WORKLOAD, "mode": args.mode, "tenants_per_gpu": TENANTS,
-                       "partition_bytes": PART, "copy_bytes": COPY_BYTES, "saxpy_n": SAXPY_N,
-                       "l2": "inputs larger than L2 (4 GiB per tensor vs 126 MB L2), no flush",
-                       "parallelism": f"{world} GPU(s), one arena per GPU, tenants sharded, no data-path collective"},
+            "config": gpu_config(args.mode, world),
             "per_gpu_GBps": round(value / world, 1),
             "frac_of_hbm_peak": round(value / world / hbm, 4),
             "parity": parity["status"], "parity_detail": parity,
@@ -1058,14 +1063,15 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": round(1e3 * el / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (NumPy PCG64 seeded 1000*2+tenant)",
-        "config": {"workload": WORKLOAD, "mode": args.mode, "tenants_per_gpu": TENANTS,
-                   "partition_bytes": PART, "copy_bytes": COPY_BYTES, "saxpy_n": SAXPY_N,
-                   "sample_run": {"tenants": th, "copy_bytes_per_tenant": SAMPLE_COPY,
-                                  "saxpy_n_per_tenant": SAMPLE_SAXPY,
-                                  "note": "each step is a bounded sample of the C2 workload above: the same kernels, "
-                                          "fence and mode over 64 MiB copies and 2^24-element saxpys per tenant "
-                                          "(the value is GB/s of algorithmic bytes, comparable across sizes)"},
-                   "parallelism": "host threads, one tenant per thread"},
+        # the config is our arm's, key for key (the contract: the reference arm
+        # runs on our arm's config, each step a bounded sample of it); what a
+        # step really runs is stated beside it, in sample_run
+        "config": gpu_config(args.mode, world),
+        "sample_run": {"tenants": th, "copy_bytes_per_tenant": SAMPLE_COPY, "saxpy_n_per_tenant": SAMPLE_SAXPY,
+                       "parallelism": "host threads, one tenant per thread",
+                       "note": "each step is a bounded sample of the config's C2 workload: the same kernels, "
+                               "fence and mode over 64 MiB copies and 2^24-element saxpys per tenant "
+                               "(the value is GB/s of algorithmic bytes, comparable across sizes)"},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": th, "kind": "oracle",
                          "sample": f"per step {th} tenants x (64 MiB copy + 2^24-element saxpy) of the C2 workload"},

@@ -165,11 +165,16 @@ __global__ void __launch_bounds__(kThreads, 5) k_gatherD(const __grid_constant__
 //   block in none / mask / mask-count too, instead of a predicated load
 //   (mask-count D = 64: +13.2 -> +0.3 %; modulo and clamp keep the
 //   predicated load: 7-40 % slower with the selected address).
+// (the clamp knobs are bit masks over G: bit G set = applied to slots of G
+// vectors; CLAMP_SAFE needs a power-of-two slot count at G = 1)
 #ifndef GD_GATHER_CLAMP_SAFE
-#define GD_GATHER_CLAMP_SAFE 1
+#define GD_GATHER_CLAMP_SAFE 0x2
 #endif
 #ifndef GD_GATHER_CLAMP_SYNCWARP
-#define GD_GATHER_CLAMP_SYNCWARP 1
+#define GD_GATHER_CLAMP_SYNCWARP 0x16
+#endif
+#ifndef GD_GATHER_CLAMP_REDIRECT
+#define GD_GATHER_CLAMP_REDIRECT 0x0
 #endif
 #ifndef GD_GATHER_LIVE_REDIRECT
 #define GD_GATHER_LIVE_REDIRECT 1
@@ -195,6 +200,7 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
                                               uint64_t s0, uint64_t nslots, uint32_t tpr32, uint64_t dv,
                                               uint32_t &nv) {
     constexpr int S = 4 / G;
+    constexpr bool kClampSafe = ((GD_GATHER_CLAMP_SAFE >> G) & 1) && (G > 1 || P2);
     const Fence<SMODE, 4> fi(fd);
     const Fence<SMODE, 16> fo(fd);
     const Fence<TMODE, 16> ft(fd);
@@ -261,7 +267,7 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
             uint32_t ci = 0;
             const bool oki = fi.go_aligned(ai, ci, 1) && live[k];        // ALU only: no branch
             okj[k] = oki;
-            if constexpr (SMODE == kClamp && !(GD_GATHER_CLAMP_SAFE && G == 1 && P2)) {   // (clamp: only dead slots are refused)
+            if constexpr (SMODE == kClamp && !kClampSafe) {   // (clamp: only dead slots are refused)
                 j[k] = 0;
                 if (oki) j[k] = __ldg(reinterpret_cast<const int32_t *>(fi.addr(ai)));
             } else {
@@ -274,13 +280,13 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     }
     // (clamp: a warp-synchronising point after the index loads keeps ptxas
     // from consuming each loaded index before the next load issues)
-    if constexpr (TMODE == kClamp && GD_GATHER_CLAMP_SYNCWARP) __syncwarp();
+    if constexpr (TMODE == kClamp && ((GD_GATHER_CLAMP_SYNCWARP >> G) & 1)) __syncwarp();
     uint64_t at[S][G];
     bool ok[S][G];
     uint32_t cnt[S];
 #pragma unroll
     for (int k = 0; k < S; k++) {                       // 2. fenced table addresses (ALU only)
-        const int32_t jk = ((SMODE == kClamp && !(GD_GATHER_CLAMP_SAFE && G == 1 && P2)) || okj[k]) ? j[k] : 0;   // a refused index load reads 0
+        const int32_t jk = ((SMODE == kClamp && !kClampSafe) || okj[k]) ? j[k] : 0;   // a refused index load reads 0
         const uint64_t rt = table + (uint64_t)((int64_t)jk * (int64_t)rowbytes) + tv[k];   // vector g = 0
         bool whole = false;                             // every vector of the slot in / unwrapped
         uint64_t fr = rt;
@@ -318,7 +324,8 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     for (int k = 0; k < S; k++) {                       // 3. table loads
 #pragma unroll
         for (int g = 0; g < G; g++) {
-            if constexpr (GD_ZERO_REDIRECT && (TMODE == kCheck || (GD_GATHER_LIVE_REDIRECT && (TMODE == kNone ||
+            if constexpr (GD_ZERO_REDIRECT && (TMODE == kCheck || (TMODE == kClamp && ((GD_GATHER_CLAMP_REDIRECT >> G) & 1)) ||
+                                               (GD_GATHER_LIVE_REDIRECT && (TMODE == kNone ||
                                                   TMODE == kMask || TMODE == kMaskCount)))) {
                 // refused / dead: the trusted zero block (per access at D = 32:
                 // +3.8 -> +1.1 %; the predicated form stays for the other

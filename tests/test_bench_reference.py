@@ -22,6 +22,12 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in d["config"]
+    # the contract: the reference arm runs on OUR arm's config, key for key;
+    # what a bounded step really runs is stated beside it
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.gpu_config(d["config"]["mode"], 1)
+    assert d["sample_run"]["copy_bytes_per_tenant"] < d["config"]["copy_bytes"]
 
 
 def test_json_line_survives_stdout_noise():

@@ -134,9 +134,12 @@ def main():
     only = set(args.only.split(",")) if args.only else None
     hbm, bf16, bf16s = peaks()
     torch.cuda.set_device(0)
-    arena = g.Arena(0, 2 * PART)
-    victim = arena.partition_alloc(PART)
-    p = arena.partition_alloc(PART)
+    # KB_SLOTS=8: an 8 x 16 GiB arena (the bench's layout), the last partition
+    # timed (placement probe); default: a victim and the timed partition
+    slots = int(os.environ.get("KB_SLOTS", "2"))
+    arena = g.Arena(0, slots * PART)
+    parts = [arena.partition_alloc(PART) for _ in range(slots)]
+    victim, p = parts[0], parts[-1]
     b = p.base
     gen = torch.Generator(device="cuda:0")
     gen.manual_seed(2001)
