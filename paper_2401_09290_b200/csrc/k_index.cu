@@ -339,13 +339,30 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
         if (live[k]) nv += cnt[k];
     }
     if constexpr (TMODE == kClamp) {                    // 3b. rare: outside vectors, after every load issued
+#ifndef GD_GATHER_CLAMP_FIX_BRANCH
+#define GD_GATHER_CLAMP_FIX_BRANCH 0x0
+#endif
+        // (bit G of CLAMP_FIX_BRANCH: one branch around the whole fix-up, taken
+        // only when some vector of the thread lies outside; else predicated
+        // edge-word loads per vector.  Off: at G = 2 and 1 it makes ptxas
+        // spill within the 6-CTA register budget.  The D = 64 clamp gather
+        // stays +6-11 % over its twin, against 0-1 % for every other mode:
+        // measured variants -- index loads from a safe word, no warp sync,
+        // table loads from the zero block -- all 6-47 %, tools/r02_iter11.sh)
+        bool anyout = !((GD_GATHER_CLAMP_FIX_BRANCH >> G) & 1);
 #pragma unroll
-        for (int k = 0; k < S; k++) {
+        for (int k = 0; k < S; k++)
 #pragma unroll
-            for (int g = 0; g < G; g++) {
-                if (live[k] && !ok[k][g]) {
-                    const uint32_t w = ld_tab(ft.edge4(at[k][g]));
-                    r[k][g] = make_uint4(w, w, w, w);
+            for (int g = 0; g < G; g++) anyout = anyout || (live[k] && !ok[k][g]);
+        if (anyout) {
+#pragma unroll
+            for (int k = 0; k < S; k++) {
+#pragma unroll
+                for (int g = 0; g < G; g++) {
+                    if (live[k] && !ok[k][g]) {
+                        const uint32_t w = ld_tab(ft.edge4(at[k][g]));
+                        r[k][g] = make_uint4(w, w, w, w);
+                    }
                 }
             }
         }
