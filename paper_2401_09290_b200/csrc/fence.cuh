@@ -38,17 +38,22 @@
 #ifndef GD_ZERO_REDIRECT
 #define GD_ZERO_REDIRECT 1
 #endif
+// Modulo fence: offsets below 2 size take one conditional subtract instead
+// of the reciprocal (Fence::addr); 0 = always the reciprocal (A/B builds).
+#ifndef GD_MODULO_FAST
+#define GD_MODULO_FAST 0
+#endif
 
 namespace gd {
 
 // Per-width precomputation, hoisted out of every loop (uniform values).
 template <int MODE, int W>
 struct Fence {
-    uint64_t base, keep, size, inv, lim, zero;
+    uint64_t base, keep, size, inv, lim, zero, size2;
     uint32_t mask_hi;              // high word of size - 1 (= of keep for every W <= 16)
     __device__ __forceinline__ explicit Fence(const FenceDesc &fd)
         : base(fd.base), keep(W == 16 ? fd.mask16 : W == 4 ? fd.mask4 : fd.mask & ~(uint64_t)(W - 1)), size(fd.size),
-          inv(fd.inv), lim(fd.size - W), zero(fd.zero), mask_hi((uint32_t)(fd.mask >> 32)) {}
+          inv(fd.inv), lim(fd.size - W), zero(fd.zero), size2(2 * fd.size), mask_hi((uint32_t)(fd.mask >> 32)) {}
     // The address a load reads when `ok` may refuse it (check / clamp
     // predicate, or a dead lane): refused -> the trusted zero block, which
     // reads 0 exactly as a refused check-mode load must (reading A1).  An
@@ -62,6 +67,13 @@ struct Fence {
             return (a & keep) | base;
         } else if constexpr (MODE == kModulo) {
             const uint64_t off = a - base;
+#if GD_MODULO_FAST
+            // an offset below 2 size (every access inside the partition, and
+            // every one up to a partition past its end) needs one conditional
+            // subtract; only the others take the reciprocal (exact either
+            // way: the u64 remainder of A10)
+            if (off < size2) return base + ((off >= size ? off - size : off) & ~(uint64_t)(W - 1));
+#endif
             uint64_t r = off - __umul64hi(off, inv) * size;
             if (r >= size) r -= size;
             return base + (r & ~(uint64_t)(W - 1));

@@ -225,6 +225,7 @@ def main():
         # fence's ALU cost is least hidden (the paper's all-cache-hit worst case,
         # 28-57 % at 100 % L1 hits)
         MiB = 1 << 20
+        b = p.base + int(os.environ.get("KB_L2_OFF", "0"))   # placement probe (bench.py uses base + 1 GiB)
         devmem.view(b, 16 * MiB, torch.int32).random_(generator=gen)
         r = time_modes_batched(lambda m, s: arena.copy(p.id, m, b + 64 * MiB, b, 32 * MiB, stream=s), args.reps)
         results["l2_copy_32MiB"] = summarize("L2 copy 32 MiB", r, 2 * 32 * MiB, "GB/s", hbm)
