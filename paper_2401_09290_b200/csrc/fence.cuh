@@ -38,8 +38,10 @@
 #ifndef GD_ZERO_REDIRECT
 #define GD_ZERO_REDIRECT 1
 #endif
-// Modulo fence: offsets below 2 size take one conditional subtract instead
-// of the reciprocal (Fence::addr); 0 = always the reciprocal (A/B builds).
+// Modulo fence: with 1, offsets below 2 size take one conditional subtract
+// instead of the reciprocal (Fence::addr).  Off: the per-access branch cost
+// more than the reciprocal it saves (tools/r02_iter12.sh: row gather D = 32
+// per access +1.8 -> +9.6 %, scatter-add +4.8 -> +6.1 %, L2 saxpy +12 -> +16 %).
 #ifndef GD_MODULO_FAST
 #define GD_MODULO_FAST 0
 #endif
