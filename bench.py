@@ -648,6 +648,8 @@ def run_gpu(args):
     sx_ms, sx_bytes = solo[("saxpy", args.mode)]
     achieved = sx_bytes / (sx_ms / 1e3) / 1e9
     mode_id = ALL_MODES.index(args.mode)
+    if args.mode == "mask" and ncu_traffic("k_saxpy<6>")[0] is not None:
+        mode_id = 6          # mask on a >= 4 GiB partition launches k_saxpy<kMaskBig> (fence_desc.h)
     traffic, dram_pct, traffic_src = ncu_traffic(f"k_saxpy<{mode_id}>")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic,

@@ -67,6 +67,8 @@ struct Fence {
     __device__ __forceinline__ uint64_t addr(uint64_t a) const {
         if constexpr (MODE == kMask || MODE == kMaskCount) {
             return (a & keep) | base;
+        } else if constexpr (MODE == kMaskBig) {      // a W-aligned (the call sites' vectors and tails)
+            return addr_big(a);
         } else if constexpr (MODE == kModulo) {
             const uint64_t off = a - base;
 #if GD_MODULO_FAST

@@ -4,7 +4,10 @@
 
 namespace gd {
 
-enum Mode : int { kNone = 0, kMask = 1, kCheck = 2, kModulo = 3, kMaskCount = 4, kClamp = 5 };
+enum Mode : int { kNone = 0, kMask = 1, kCheck = 2, kModulo = 3, kMaskCount = 4, kClamp = 5,
+                  // internal: MASK on a kBig partition (Fence::addr_big, one LOP3), chosen by the
+                  // launchers of the streaming kernels from FenceDesc::flags; never an API mode
+                  kMaskBig = 6 };
 
 // modes that count accesses outside the partition (the trusted counter)
 constexpr bool counts(int m) { return m == kCheck || m == kMaskCount || m == kClamp; }

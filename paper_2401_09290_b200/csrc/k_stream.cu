@@ -246,7 +246,8 @@ cudaError_t launch_copy(int mode, const FenceDesc &fd, uint64_t dst, uint64_t sr
                         cudaStream_t s, const Geom &) {
     switch (mode) {
         case kNone: return copy_t<kNone>(fd, dst, src, nbytes, s);
-        case kMask: return copy_t<kMask>(fd, dst, src, nbytes, s);
+        case kMask:
+            return (fd.flags & kBig) ? copy_t<kMaskBig>(fd, dst, src, nbytes, s) : copy_t<kMask>(fd, dst, src, nbytes, s);
         case kModulo: return copy_t<kModulo>(fd, dst, src, nbytes, s);
         case kMaskCount: return copy_t<kMaskCount>(fd, dst, src, nbytes, s);
         case kClamp: return copy_t<kClamp>(fd, dst, src, nbytes, s);
@@ -258,7 +259,8 @@ cudaError_t launch_saxpy(int mode, const FenceDesc &fd, float alpha, uint64_t x,
                          cudaStream_t s, const Geom &) {
     switch (mode) {
         case kNone: return saxpy_t<kNone>(fd, alpha, x, y, n, s);
-        case kMask: return saxpy_t<kMask>(fd, alpha, x, y, n, s);
+        case kMask:
+            return (fd.flags & kBig) ? saxpy_t<kMaskBig>(fd, alpha, x, y, n, s) : saxpy_t<kMask>(fd, alpha, x, y, n, s);
         case kModulo: return saxpy_t<kModulo>(fd, alpha, x, y, n, s);
         case kMaskCount: return saxpy_t<kMaskCount>(fd, alpha, x, y, n, s);
         case kClamp: return saxpy_t<kClamp>(fd, alpha, x, y, n, s);

@@ -14,7 +14,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "paper_2401_09290_b200", "build")
-MODES = {"0": "none", "1": "mask", "2": "check", "3": "modulo", "4": "maskcount", "5": "clamp"}
+MODES = {"0": "none", "1": "mask", "2": "check", "3": "modulo", "4": "maskcount", "5": "clamp",
+         "6": "mask_big"}  # 6: internal, mask on a >= 4 GiB partition (fence_desc.h kMaskBig)
 
 
 def demangle(names):

@@ -19,7 +19,7 @@ def main(path, out):
         name = re.sub(r"<.*>", "", re.sub(r"^.*::", "", r[ki].split("(")[0]))
         m = re.search(r"<(\d)>", r[ki])
         if "<" in r[ki] and m:
-            name += f"<{ {'0': 'none', '1': 'mask', '2': 'check', '3': 'modulo', '4': 'maskcount', '5': 'clamp'}[m.group(1)] }>"
+            name += f"<{ {'0': 'none', '1': 'mask', '2': 'check', '3': 'modulo', '4': 'maskcount', '5': 'clamp', '6': 'mask_big'}[m.group(1)] }>"
         d = agg.setdefault(name, {"launches": 0, "total_ns": 0.0, "grid": r[gi]})
         d["launches"] += 1
         d["total_ns"] += float(r[vi].replace(",", ""))
@@ -29,7 +29,10 @@ def main(path, out):
         d["share"] = round(d["total_ns"] / tot, 4)
     # share of each kernel within the timed bench step (C2, mask: one copy and
     # one saxpy per tenant): what bench.py's roofline.share_of_step measures live
-    step = [k for k in ("k_copy<mask>", "k_saxpy<mask>") if k in agg]
+    # (mask on the bench's 16 GiB partitions launches the internal mask_big
+    # instantiation, fence_desc.h kMaskBig)
+    step = [k for k in ("k_copy<mask>", "k_saxpy<mask>") if k in agg] or \
+        [k for k in ("k_copy<mask_big>", "k_saxpy<mask_big>") if k in agg]
     step_tot = sum(agg[k]["mean_us"] for k in step)
     step_share = {k: round(agg[k]["mean_us"] / step_tot, 4) for k in step} if step_tot else {}
     json.dump({"source": path, "note": "ncu --metrics gpu__time_duration.sum --clock-control none; cold-cache, "
