@@ -321,13 +321,20 @@ __device__ __forceinline__ void strip(const FenceDesc &fd, uint64_t out, uint64_
 }
 
 // The strip of a warp's rows: full (ROWS rows, every lane interior: the common
-// case) or not (the grid's last rows, its first / last columns).
+// case) or not (the grid's last rows, its first / last columns).  Full strips
+// on a kBig partition take the BIG variant (one-LOP3 partition test and mask
+// fence), except mask-count: with 16-row strips ptxas spills at 64
+// registers, and with 8-row strips it measured no faster (L2-resident 2048^2
+// per access +23.9 % vs +22.6 %, tools/r02_iter14.sh; knob kept for A/B).
+#ifndef GD_STENCIL_MC_BIG8
+#define GD_STENCIL_MC_BIG8 0
+#endif
 template <int MODE, int kG, int ROWS, bool WALK = false>
 __device__ __forceinline__ void strip_rows(const FenceDesc &fd, uint64_t out, uint64_t in, uint32_t W,
                                            uint64_t pitch, float c0, float c1, uint64_t c, uint32_t r0, uint32_t r1,
                                            uint32_t &nv) {
     if (r1 - r0 == ROWS && (!GD_STENCIL_FULL_WARP || __all_sync(0xffffffffu, c >= 1 && c + 5 <= W))) {
-        if (((counts(MODE) && MODE != kMaskCount) || MODE == kMask) && (fd.flags & kBig))
+        if (((counts(MODE) && (MODE != kMaskCount || (GD_STENCIL_MC_BIG8 && ROWS <= 8))) || MODE == kMask) && (fd.flags & kBig))
             strip<MODE, kG, ROWS, true, WALK, true>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);
         else
             strip<MODE, kG, ROWS, true, WALK>(fd, out, in, W, pitch, c0, c1, c, r0, r1, nv);

@@ -277,6 +277,68 @@ def test_c4_stencil_full_in_crossing_end(arenas, mode):
         np.testing.assert_array_equal(got, want, err_msg=f"row {r}")
 
 
+@pytest.mark.parametrize("side", ["in", "out"])
+@pytest.mark.parametrize("mode", ["mask", "check", "modulo", "maskcount", "clamp"])
+def test_stencil_small_grid_big_partition_crossing(arenas, side, mode):
+    """The L2-resident size (2048^2: 8-row strips) in a 16 GiB partition, so
+    the >= 4 GiB code paths of the small-grid kernels run (one-LOP3 partition
+    test, mask fence on the high word walking fenced pointers, mask-count's
+    BIG variant), with `in` or `out` crossing the partition end by 64 rows:
+    EVERY row against the oracle's stencil over its 3-row band (resolved per
+    mode as in test_c4_stencil_full_in_crossing_end; a refused or wrapped
+    output row as in test_c4_stencil_full_out_crossing_end), and the exact
+    count.  Hoisted here, per access via test_gpu_peraccess.py."""
+    a = arenas(PART)
+    p = a.partition_alloc(PART)
+    H = W = 2048
+    rb = 4 * W
+    if side == "in":
+        inp, out = p.end - (H - 64) * rb, p.base + 4 * GiB
+    else:
+        inp, out = p.base + 4 * GiB, p.end - (H - 64) * rb
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(4003)
+    n_in = (H - 64) * W if side == "in" else H * W
+    devmem.view(inp, n_in, torch.float32).uniform_(0, 1, generator=gen)
+    devmem.view(p.base, 64 * W, torch.float32).uniform_(0, 1, generator=gen)       # wrap target of `in`
+    torch.cuda.synchronize()
+    a.stats_reset()
+    a.stencil(p.id, mode, out, inp, H, W, W, 0.5, 0.125)
+    v = a.stats(p.id)["violations"]
+    counting = mode in ("check", "maskcount", "clamp")
+    if side == "in":
+        assert v == ((W - 2) * (64 + 3 * 63 + 62) if counting else 0)
+    else:
+        assert v == (63 * (W - 2) if counting else 0)
+    inside_in = download(inp, n_in * 4)                                          # the rows inside
+    wrap = download(p.base, 64 * rb)
+    last = download(p.end - 4, 4)
+
+    def in_row(x):
+        if inp + (x + 1) * rb <= p.end:
+            return inside_in[x * rb:(x + 1) * rb]
+        if mode == "check":
+            return np.zeros(rb, np.uint8)
+        if mode == "clamp":
+            return np.tile(last, W)
+        o = (inp + x * rb - p.base) % p.size                                     # mask = modulo (pow2)
+        return wrap[o:o + rb]
+
+    for r in range(1, H - 1):
+        band = np.concatenate([in_row(x) for x in (r - 1, r, r + 1)])
+        m = oracle.Mem(0x20000000, 1 << 16)
+        m.buf[:band.size] = band
+        oracle.stencil(m, 0x20000000, 1 << 16, "none", 0x20000000 + (1 << 15), 0x20000000, 3, W, W, 0.5, 0.125)
+        want = m.view(0x20000000 + (1 << 15) + rb, np.uint32, W)[1:W - 1]
+        dst = out + r * rb
+        if dst + rb <= p.end:
+            got = download(dst, rb).view(np.uint32)[1:W - 1]
+            np.testing.assert_array_equal(got, want, err_msg=f"row {r}")
+        elif mode in ("mask", "modulo", "maskcount"):
+            got = download(p.base + (dst - p.base) % p.size, rb).view(np.uint32)[1:W - 1]
+            np.testing.assert_array_equal(got, want, err_msg=f"row {r} (wrapped)")
+
+
 def test_c4_stencil_v2_full_sampled_rows(arenas):
     """K5 v2 at the BASELINE size in the bench's launch configuration: sampled
     rows (incl. tile edges at 16-row and 248-column boundaries) against the
