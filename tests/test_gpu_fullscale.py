@@ -169,6 +169,78 @@ def test_c2_copy_saxpy_full(arenas, mode):
     np.testing.assert_array_equal(got.view(np.uint32), m.view(0x10000000 + (4 << 20), np.uint32, 1 << 20))
 
 
+@pytest.mark.parametrize("mode", ["mask", "check", "modulo", "maskcount", "clamp"])
+def test_c2_full_crossing_end(arenas, mode):
+    """SURVEY.md §8(d) C2 parity variant at the bench size: src / x at 4 GiB,
+    dst / y at 12 GiB + 1 MiB, so the last 1 MiB of dst / y crosses the end of
+    the 16 GiB partition (the >= 4 GiB mask path, kMaskBig, walks into it).
+    Mask / modulo / mask-count wrap it into offsets [0, 1 MiB), which nothing
+    else touches (race-free); check refuses and counts it (65,536 16-byte
+    stores; 2 x 262,144 y accesses); clamp counts like check.  Checked: the
+    whole wrapped MiB and the last inside MiB of the copy, the counts, and
+    2^20 sampled saxpy elements plus every wrapped one against the oracle."""
+    a = arenas(PART)
+    p = a.partition_alloc(PART)
+    MiB = 1 << 20
+    src = x = p.base + 4 * GiB
+    dst = y = p.base + 12 * GiB + MiB
+    n = 1 << 30
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(2003)
+    devmem.view(src, GiB, torch.int32).random_(generator=gen)
+    devmem.view(p.base, MiB // 4, torch.float32).uniform_(-1, 1, generator=gen)       # the wrap target
+    wrap0 = download(p.base, MiB)
+    counting = mode in ("check", "maskcount", "clamp")
+    # copy
+    a.stats_reset()
+    a.copy(p.id, mode, dst, src, 4 * GiB)
+    assert a.stats(p.id)["violations"] == (MiB // 16 if counting else 0)
+    tail_in = download(src + 4 * GiB - 2 * MiB, 2 * MiB)          # the source of the last inside / outside MiB
+    last_in = download(p.end - MiB, MiB)
+    if mode == "clamp":       # the last 16-byte unit: the copy's clamped unit stores collide there (R-race)
+        np.testing.assert_array_equal(last_in[:-16], tail_in[:MiB - 16])
+    else:
+        np.testing.assert_array_equal(last_in, tail_in[:MiB])
+    wrapped = download(p.base, MiB)
+    if mode in ("mask", "modulo", "maskcount"):
+        np.testing.assert_array_equal(wrapped, tail_in[MiB:])
+    elif mode == "check":
+        np.testing.assert_array_equal(wrapped, wrap0)             # nothing landed
+    # saxpy (x = the copy's source as floats: finite values are all that matters;
+    # y starts as what the copy wrote inside and as wrap0 wrapped)
+    devmem.view(x, n, torch.float32).uniform_(-1, 1, generator=gen)
+    devmem.view(y, n - MiB // 4, torch.float32).uniform_(-1, 1, generator=gen)
+    devmem.view(p.base, MiB // 4, torch.float32).uniform_(-1, 1, generator=gen)
+    xv = devmem.view(x, n, torch.float32)
+    yv_in = devmem.view(y, n - MiB // 4, torch.float32)
+    rng = synth.rng_for(11)
+    s_in = torch.from_numpy(np.unique(np.concatenate([rng.integers(0, n - MiB // 4, 1 << 20),
+                                                      np.arange(n - MiB // 4 - 4096, n - MiB // 4)]))).cuda()
+    if mode == "clamp":
+        s_in = s_in[s_in != n - MiB // 4 - 1]                      # the edge word: clamped stores collide (R-race)
+    xs, ys = xv[s_in].cpu().numpy(), yv_in[s_in].cpu().numpy()
+    x_tail = xv[n - MiB // 4:].cpu().numpy()
+    y_wrap0 = download(p.base, MiB).view(np.float32).copy()
+    a.stats_reset()
+    a.saxpy(p.id, mode, 1.5, x, y, n)
+    assert a.stats(p.id)["violations"] == (2 * (MiB // 4) if counting else 0)
+
+    def oracle_saxpy(xa, ya):
+        k = xa.size
+        m = oracle.Mem(0x10000000, 8 * k + 64)
+        m.write(0x10000000, xa)
+        m.write(0x10000000 + 4 * k, ya)
+        oracle.saxpy(m, 0x10000000, 8 * k + 64, "none", 1.5, 0x10000000, 0x10000000 + 4 * k, k)
+        return m.view(0x10000000 + 4 * k, np.uint32, k)
+
+    np.testing.assert_array_equal(yv_in[s_in].cpu().numpy().view(np.uint32), oracle_saxpy(xs, ys))
+    got_wrap = download(p.base, MiB).view(np.uint32)
+    if mode in ("mask", "modulo", "maskcount"):
+        np.testing.assert_array_equal(got_wrap, oracle_saxpy(x_tail, y_wrap0))
+    elif mode == "check":
+        np.testing.assert_array_equal(got_wrap, y_wrap0.view(np.uint32))
+
+
 def test_c4_stencil_full_sampled_rows(arenas):
     a = arenas(PART)
     p = a.partition_alloc(PART)

@@ -19,7 +19,7 @@ def test_parity_suites_with_per_access_fencing():
            "tests/test_gpu_kernels.py", "tests/test_gpu_count_modes.py", "tests/test_gpu_modulo.py",
            "tests/test_gpu_fullscale.py",
            "-k", "crossing or adversarial or straddle or victim or in_bounds or c1_toy or scatter or stencil or walk "
-           "or c3_gather_full or c2_copy_saxpy_full"]
+           "or c3_gather_full or c2_copy_saxpy_full or c2_full_crossing"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
