@@ -36,6 +36,9 @@ __device__ __forceinline__ uint64_t row_addr(uint64_t table, int32_t j) {
     return table + (uint64_t)((int64_t)j * 4);        // sext, scale in 64 bits
 }
 
+// (A range-only table test, with the one-LOP3 form on >= 4 GiB partitions,
+// measured slower at the L2-resident size: clamp +1.4 -> +11.3 %, per-access
+// check +3.2 -> +4.1 %, tools/r02_iter15.sh; not used.)
 template <int MODE>
 __device__ __forceinline__ uint32_t fenced_tab(const Fence<MODE, 4> &f4, uint64_t table, int32_t j, uint32_t &nv) {
     const uint64_t a = row_addr(table, j);
