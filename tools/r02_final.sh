@@ -32,9 +32,9 @@ cap() {  # name, kernel regex, prof_kernel args...
 for m in none mask check; do
   cap copy_$m k_copy --kind copy --mode $m
   cap saxpy_$m k_saxpy --kind saxpy --mode $m
-  cap gather_$m k_gather1 --kind gather --mode $m
-  cap scatterA3_$m "k_scatter_part<\d, 1>" --kind scatter --mode $m
-  cap scatterB_$m k_scatter_apply --kind scatter --mode $m
+  cap gather_$m "k_gather1<" --kind gather --mode $m --oob 0
+  cap scatterA3_$m "k_scatter_part<.int.[0-9], .int.1>" --kind scatter --mode $m --oob 0
+  cap scatterB_$m k_scatter_apply --kind scatter --mode $m --oob 0
   cap stencil_$m "k_stencil<" --kind stencil --mode $m
   cap stenciltma_$m k_stencil_tma --kind stencil_tma --mode $m
   cap gatherrows_$m k_gatherR --kind gatherrows --D 32 --mode $m
