@@ -98,8 +98,12 @@ typedef enum {
 /* Per-access flag, OR-ed into the mode of any launch (gd_launch_fenced_*,
  * gd_work.mode): fence every access one by one, as the paper's instrumented
  * kernels do ("before every load and store"; §4.3), instead of
- * the default tile-level range test that runs the unfenced body on tiles
- * wholly inside the partition (reading R-hoist).  Results and
+ * the default hoisting: a CHECK / MODULO / MASK_COUNT / CLAMP launch of copy,
+ * saxpy or stencil v1 whose whole footprint lies in the partition runs the
+ * unfenced twin (decided on the host from the launch's bounds snapshot,
+ * DESIGN.md reading R-hoist-launch), and inside other launches a tile-level
+ * range test runs the unfenced body on tiles wholly inside the partition
+ * (reading R-hoist).  Results and
  * violation counts are identical either way; only the cost differs.  The
  * descriptor-fenced TMA kernels (GEMM, K5 v2) have no per-access fence and
  * ignore it; MASK is always per access.  Setting GD_CHECK_PER_ACCESS=1 in the
