@@ -45,8 +45,14 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kU = 4;                                  // 16-byte index vectors per thread
 constexpr uint64_t kChunk = (uint64_t)kThreads * kU;   // vectors (4 indices each) per CTA
-constexpr int kSliceShift = 25;                        // 32 MiB slices
-constexpr uint32_t kMaxSlices = 512;                   // partitions up to 16 GiB (u32 word offsets)
+#ifndef GD_SCATTER_SLICE_SHIFT
+#define GD_SCATTER_SLICE_SHIFT 25
+#endif
+// 32 MiB slices: measured 784 GB/s against 746 (16 MiB) and 631 (64 MiB),
+// and 689 without the L2 bulk prefetch (tools/r02_iter16.sh)
+constexpr int kSliceShift = GD_SCATTER_SLICE_SHIFT;
+constexpr uint32_t kMaxSlices = (uint32_t)((1ull << 34) >> kSliceShift);   // partitions up to 16 GiB (u32 word offsets)
+static_assert(kMaxSlices >= kThreads && kMaxSlices % kThreads == 0 && kMaxSlices <= 1024, "slice count");
 
 __device__ __forceinline__ uint4 ld_u4(uint64_t a) { return __ldcs(reinterpret_cast<const uint4 *>(a)); }
 __device__ __forceinline__ uint32_t ld_w(uint64_t a) { return __ldcs(reinterpret_cast<const unsigned int *>(a)); }
@@ -231,8 +237,14 @@ __global__ void __launch_bounds__(kThreads) k_scatter_part(const __grid_constant
         __shared__ unsigned wsum[kThreads / 32];
         __shared__ uint2 staged[kThreads * kItems];
         const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
-        const uint32_t a0 = 2 * t < nslices ? hist[2 * t] : 0u, a1 = 2 * t + 1 < nslices ? hist[2 * t + 1] : 0u;
-        uint32_t run = a0 + a1;                        // inclusive scan, two slices per thread
+        constexpr uint32_t SPT = kMaxSlices / kThreads;             // slices per thread
+        uint32_t a[SPT], sum = 0;
+#pragma unroll
+        for (uint32_t q = 0; q < SPT; q++) {
+            a[q] = SPT * t + q < nslices ? hist[SPT * t + q] : 0u;
+            sum += a[q];
+        }
+        uint32_t run = sum;                            // inclusive scan, SPT slices per thread
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, run, o);
@@ -247,9 +259,12 @@ __global__ void __launch_bounds__(kThreads) k_scatter_part(const __grid_constant
             pre += k < warp ? wsum[k] : 0u;
             total += wsum[k];
         }
-        const uint32_t ex = pre + run - (a0 + a1);
-        if (2 * t < nslices) lstart[2 * t] = ex;
-        if (2 * t + 1 < nslices) lstart[2 * t + 1] = ex + a0;
+        uint32_t ex = pre + run - sum;
+#pragma unroll
+        for (uint32_t q = 0; q < SPT; q++) {
+            if (SPT * t + q < nslices) lstart[SPT * t + q] = ex;
+            ex += a[q];
+        }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kItems; k++)
@@ -301,7 +316,10 @@ __global__ void __launch_bounds__(kThreads) k_scatter_apply(uint64_t base, uint6
                                                             const unsigned *lim) {
     const uint64_t n = *total;
     const uint64_t c0 = (uint64_t)blockIdx.x * kThreads * 4;
-    if (threadIdx.x == 0 && c0 < n) {
+#ifndef GD_SCATTER_PREFETCH
+#define GD_SCATTER_PREFETCH 1
+#endif
+    if (GD_SCATTER_PREFETCH && threadIdx.x == 0 && c0 < n) {
         const uint32_t s = pairs[c0].x >> (kSliceShift - 2);             // the slice of the CTA's first update
         const uint64_t e = lim[s], c = cnt[s], st = e - c;
         const auto prefetch = [&](uint32_t sl, uint64_t from) {
