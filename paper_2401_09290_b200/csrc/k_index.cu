@@ -12,9 +12,8 @@
 // output stores.  In the hoistable modes (check, modulo, mask-count, clamp)
 // the index and output streams are range-tested once per CTA chunk (fence.cuh
 // range_in); the random table accesses are fenced one by one.  D % 4 == 0 with 16-byte-aligned table and output:
-// row slots of 128-bit vectors (k_gatherR below).  Other D > 1: one warp per
-// index row, lanes stride over the row; lane 0 loads the index once (one
-// logical access, as in the oracle) and broadcasts it.
+// row slots of 128-bit vectors (k_gatherR below).  Other D > 1: the n * D
+// output words as one flat stream (k_gatherE below).
 #include "fence.cuh"
 #include "kernels.h"
 
@@ -114,30 +113,103 @@ __global__ void __launch_bounds__(kThreads, 5) k_gather1(const __grid_constant__
 }
 
 // ---------------------------------------------------------------------------
-// K3, D > 1: out[i*D+d] = table[sext(idx[i])*D + d]; one warp per row i.
+// K3, D >= 2 outside the row-slot path (D % 4 != 0, or table / out not
+// 16-byte aligned): out[e] = table[sext(idx[e / D]) * D + e % D] over the
+// n * D output words as one flat stream.  Each thread takes kE words kThreads
+// apart (every warp instruction covers 32 consecutive words: coalesced
+// stores, and the table words of a row are contiguous), with every index
+// load of the batch issued before the table loads and every table load
+// before the stores.  The row and column of a thread's first word come from
+// the reciprocal dinv = floor(2^64 / D) (mulhi is e / D or one less, one
+// compare finishes it), the next ones by adding kThreads / D and
+// kThreads % D.  Logical accesses as in the oracle (or_gather): one index
+// load per row, counted by the row's d == 0 word (the other words of the row
+// repeat the same fenced load and the same decision, uncounted), D table
+// loads and D stores per row.  A refused or dead load reads the trusted zero
+// block (Fence::ld_at), so no load of a batch waits on a branch.
 // ---------------------------------------------------------------------------
+constexpr int kE = 8;                                  // words per thread
+constexpr uint64_t kEChunk = (uint64_t)kThreads * kE;  // words per CTA
+// clamp holds each word's clamped table address until its load: 4 words per
+// pass (two passes per chunk) keep it free of local memory
+constexpr int ke_pass(int mode) { return mode == kClamp ? 4 : kE; }
+
+// e / D from dinv = floor(2^64 / D), D >= 2 (no 64-bit division call)
+__device__ __forceinline__ uint64_t div_d(uint64_t e, uint32_t D, uint64_t dinv) {
+    const uint64_t q = __umul64hi(e, dinv);
+    return e - q * D >= D ? q + 1 : q;
+}
+
+template <int SMODE, int TMODE, int KE>
+__device__ __forceinline__ void gathere_pass(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t idx,
+                                              uint64_t e0, uint64_t N, uint32_t D, uint64_t dinv, uint32_t qs,
+                                              uint32_t rs, uint32_t &nv) {
+    const Fence<SMODE, 4> fs(fd);
+    const Fence<TMODE, 4> ft(fd);
+    uint64_t i = div_d(e0, D, dinv);
+    uint32_t d = (uint32_t)(e0 - i * D);
+    int32_t j[KE];
+    uint32_t dd[KE];
+#pragma unroll
+    for (int u = 0; u < KE; u++) {
+        const bool live = e0 + (uint64_t)u * kThreads < N;
+        const uint64_t ai = idx + 4 * i;
+        const bool o = fs.go(ai, nv, (live && d == 0) ? 1u : 0u);
+        j[u] = (int32_t)__ldg(reinterpret_cast<const unsigned int *>(fs.ld_at(fs.addr(ai), o && live)));
+        dd[u] = d;
+        i += qs;
+        d += rs;
+        if (d >= D) {
+            d -= D;
+            i++;
+        }
+    }
+    uint32_t r[KE];
+#pragma unroll
+    for (int u = 0; u < KE; u++) {
+        const bool live = e0 + (uint64_t)u * kThreads < N;
+        const uint64_t at = table + (uint64_t)((int64_t)j[u] * (int64_t)D + (int64_t)dd[u]) * 4u;
+        const bool o = ft.go(at, nv, live ? 1u : 0u);
+        r[u] = ld_tab(ft.ld_at(ft.addr(at), o && live));
+    }
+#pragma unroll
+    for (int u = 0; u < KE; u++) {
+        const uint64_t e = e0 + (uint64_t)u * kThreads;
+        if (e < N) {
+            const uint64_t ao = out + 4 * e;
+            if (fs.go(ao, nv, 1)) st_w(fs.addr(ao), r[u]);
+        }
+    }
+}
+
+template <int SMODE, int TMODE>
+__device__ __forceinline__ void gathere_chunk(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t idx,
+                                              uint64_t e0, uint64_t N, uint32_t D, uint64_t dinv, uint32_t qs,
+                                              uint32_t rs, uint32_t &nv) {
+    constexpr int KE = ke_pass(TMODE);
+#pragma unroll 1
+    for (int p = 0; p < kE; p += KE)
+        gathere_pass<SMODE, TMODE, KE>(fd, out, table, idx, e0 + (uint64_t)p * kThreads, N, D, dinv, qs, rs, nv);
+}
+
+// CTAs per SM: the most at which ptxas keeps the mode free of local memory
+// (none / mask / modulo 40 registers, check / mask-count / clamp 48)
+constexpr int gathere_minb(int mode) { return (mode == kCheck || mode == kMaskCount || mode == kClamp) ? 5 : 6; }
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 5) k_gatherD(const __grid_constant__ FenceDesc fd, uint64_t out,
-                                                      uint64_t table, uint64_t idx, uint64_t n, uint32_t D) {
-    const Fence<MODE, 4> f4(fd);
+__global__ void __launch_bounds__(kThreads, gathere_minb(MODE)) k_gatherE(const __grid_constant__ FenceDesc fd, uint64_t out,
+                                                      uint64_t table, uint64_t idx, uint64_t N, uint32_t D,
+                                                      uint64_t dinv, uint32_t qs, uint32_t rs) {
     uint32_t nv = 0;
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t W = (uint64_t)gridDim.x * (kThreads / 32);
-    for (uint64_t i = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; i < n; i += W) {
-        int32_t j = 0;
-        if (lane == 0) {
-            const uint64_t ai = idx + 4 * i;
-            if (f4.go(ai, nv, 1)) j = *reinterpret_cast<const int32_t *>(f4.addr(ai));
-        }
-        j = __shfl_sync(0xffffffffu, j, 0);
-        for (uint32_t d = lane; d < D; d += 32) {
-            const uint64_t e = (uint64_t)((int64_t)j * (int64_t)D + (int64_t)d);
-            const uint64_t at = table + e * 4;
-            uint32_t r = 0;
-            if (f4.go(at, nv, 1)) r = ld_tab(f4.addr(at));
-            const uint64_t ao = out + 4 * (i * D + d);
-            if (f4.go(ao, nv, 1)) *reinterpret_cast<uint32_t *>(f4.addr(ao)) = r;
-        }
+    const uint64_t c0 = (uint64_t)blockIdx.x * kEChunk, e0 = c0 + threadIdx.x;
+    if constexpr (hoistable(MODE)) {     // the index / output streams hoisted per CTA; table words fenced
+        const uint64_t cn = N - c0 < kEChunk ? N - c0 : kEChunk;
+        const uint64_t r0 = div_d(c0, D, dinv), r1 = div_d(c0 + cn - 1, D, dinv);   // rows this CTA touches
+        if (range_in(fd, idx + 4 * r0, 4 * (r1 - r0 + 1)) && range_in(fd, out + 4 * c0, 4 * cn))
+            gathere_chunk<kNone, MODE>(fd, out, table, idx, e0, N, D, dinv, qs, rs, nv);
+        else
+            gathere_chunk<MODE, MODE>(fd, out, table, idx, e0, N, D, dinv, qs, rs, nv);
+    } else {
+        gathere_chunk<MODE, MODE>(fd, out, table, idx, e0, N, D, dinv, qs, rs, nv);
     }
     if constexpr (counts(MODE)) flush_violations(nv, fd.viol);
 }
@@ -394,11 +466,19 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     }
 }
 
-// 6 CTAs (48 warps) per SM: the row gather is bound by loads in flight, and
-// 5 CTAs measured 27-41 % slower at D = 32 / 64; clamp with G = 4 needs the
-// registers of 5 (no local memory) and loses nothing there (D >= 128).
+// CTAs per SM: the row gather is bound by loads in flight (5 CTAs measured
+// 27-41 % slower than 6 at D = 32 / 64).  8 (32 registers, the unfenced
+// twin's occupancy) wherever ptxas fits the mode in 32 registers with no
+// local memory; modulo (it spills at 32 for G = 1 / 2) and clamp need more
+// (6; clamp with G = 4: 5, which loses nothing there, D >= 128).
+#ifndef GD_GATHERR_MINB8
+#define GD_GATHERR_MINB8 1
+#endif
+constexpr int gatherr_minb(int mode, int g) {
+    return mode == kClamp ? (g == 4 ? 5 : 6) : (!GD_GATHERR_MINB8 || mode == kModulo) ? 6 : 8;
+}
 template <int MODE, int G, bool P2>
-__global__ void __launch_bounds__(kThreads, (MODE == kClamp && G == 4) ? 5 : 6) k_gatherR(const __grid_constant__ FenceDesc fd, uint64_t out,
+__global__ void __launch_bounds__(kThreads, gatherr_minb(MODE, G)) k_gatherR(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                       uint64_t table, uint64_t idx, uint64_t nslots, uint32_t tpr,
                                                       uint64_t dv) {
     constexpr uint64_t ch = (uint64_t)kThreads * (4 / G);
@@ -564,9 +644,9 @@ cudaError_t gather_t(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t
             else k_gatherR<MODE, 1, false><<<grid, kThreads, 0, s>>>(fd, out, table, idx, nslots, tpr, inv);
         }
     } else {
-        static const int bps = blocks_per_sm(k_gatherD<MODE>);
-        const uint64_t want = (n * 32 + kThreads - 1) / kThreads, cap = (uint64_t)g.sms * bps;
-        k_gatherD<MODE><<<(unsigned)(want < cap ? want : cap), kThreads, 0, s>>>(fd, out, table, idx, n, D);
+        const uint64_t N = n * D;                       // (n * D < 2^64: the API bounds the output bytes)
+        if (N) k_gatherE<MODE><<<(unsigned)((N + kEChunk - 1) / kEChunk), kThreads, 0, s>>>(
+                   fd, out, table, idx, N, D, recip64(D), (uint32_t)(kThreads / D), (uint32_t)(kThreads % D));
     }
     return cudaGetLastError();
 }

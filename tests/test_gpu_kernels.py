@@ -194,10 +194,10 @@ def test_gather_adversarial(arenas, mode, frac):
 
 
 @pytest.mark.parametrize("mode", MODES[1:])
-@pytest.mark.parametrize("D", [2, 3, 33, 4, 8, 32, 64, 128, 132, 136])     # D % 4 == 0: 128-bit row slots
+@pytest.mark.parametrize("D", [2, 3, 6, 7, 33, 257, 4, 8, 32, 64, 128, 132, 136])   # D % 4 == 0: 128-bit row slots
 def test_gather_rows(arenas, mode, D):
     a, parts, rng = _setup(arenas, seed=9)
-    n = 5000 + D
+    n = min(5000 + D, (PAT_LO - OUT_OFF) // (4 * D))        # out stays below the wrapped reads (race-free)
     p = parts[1]
     j, pos = _gather_inputs(rng, n, 0.02, D)
     upload(p.base + IDX_OFF, j)
@@ -205,6 +205,23 @@ def test_gather_rows(arenas, mode, D):
          lambda p: a.gather(p.id, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, n, D),
          lambda m, p: oracle.gather(m, p.base, p.size, mode, p.base + OUT_OFF, p.base, p.base + IDX_OFF, n, D),
          None if mode == "mask" else len(pos) * D)
+
+
+@pytest.mark.parametrize("mode", MODES[1:])
+@pytest.mark.parametrize("D", [8, 32])
+def test_gather_rows_unaligned_flat(arenas, mode, D):
+    """D % 4 == 0 but the table only 4-byte aligned (idx and out must be
+    16-byte aligned, GD_ERR_ALIGN): the flat word kernel (k_gatherE) instead
+    of the 128-bit row slots, with planted rows outside the partition."""
+    a, parts, rng = _setup(arenas, seed=29)
+    n = 4099
+    p = parts[1]
+    j, pos = _gather_inputs(rng, n, 0.02, D)
+    j = np.where(j == TAB_N // D - 1, j - 1, j).astype(np.int32)  # the table starts 4 bytes in
+    upload(p.base + IDX_OFF, j)
+    _run(a, parts, 1, mode,
+         lambda p: a.gather(p.id, mode, p.base + OUT_OFF, p.base + 4, p.base + IDX_OFF, n, D),
+         lambda m, p: oracle.gather(m, p.base, p.size, mode, p.base + OUT_OFF, p.base + 4, p.base + IDX_OFF, n, D))
 
 
 @pytest.mark.parametrize("mode", ["mask", "check", "modulo"])

@@ -124,7 +124,7 @@ def test_modulo_stencil_out_crossing_end(arenas, mode):
 
 
 @pytest.mark.parametrize("mode", ["modulo", "check"])
-@pytest.mark.parametrize("D", [12, 32, 64])          # row slots: tpr 3 (reciprocal), 8 (shift); G = 1, 1, 2
+@pytest.mark.parametrize("D", [6, 12, 32, 64])       # D = 6: flat words; row slots: tpr 3 (reciprocal), 8 (shift); G = 1, 1, 2
 @pytest.mark.parametrize("case", ["out_crossing_end", "idx_below_base"])
 def test_modulo_gather_rows_stream_walk(arenas, mode, D, case):
     """Per access (run again by test_gpu_peraccess.py), the row gather fences
