@@ -131,8 +131,14 @@ __global__ void __launch_bounds__(kThreads, 5) k_gather1(const __grid_constant__
 constexpr int kE = 8;                                  // words per thread
 constexpr uint64_t kEChunk = (uint64_t)kThreads * kE;  // words per CTA
 // clamp holds each word's clamped table address until its load: 4 words per
-// pass (two passes per chunk) keep it free of local memory
-constexpr int ke_pass(int mode) { return mode == kClamp ? 4 : kE; }
+// pass (two passes per chunk) keep it free of local memory.  GD_GATHERE_NARROW:
+// the check / mask-count passes 4 words wide too, at 6 CTAs per SM instead of
+// 8 words at 5 (D = 6, tools/r02_iter22.sh: check +1.8 -> +0.3 %, mask-count
+// +5.1 -> +0.3 %, per access +6.4 -> +4.2 % / +12.8 -> +7.5 %)
+#ifndef GD_GATHERE_NARROW
+#define GD_GATHERE_NARROW 1
+#endif
+constexpr int ke_pass(int mode) { return (mode == kClamp || (GD_GATHERE_NARROW && counts(mode))) ? 4 : kE; }
 
 // e / D from dinv = floor(2^64 / D), D >= 2 (no 64-bit division call)
 __device__ __forceinline__ uint64_t div_d(uint64_t e, uint32_t D, uint64_t dinv) {
@@ -193,8 +199,10 @@ __device__ __forceinline__ void gathere_chunk(const FenceDesc &fd, uint64_t out,
 }
 
 // CTAs per SM: the most at which ptxas keeps the mode free of local memory
-// (none / mask / modulo 40 registers, check / mask-count / clamp 48)
-constexpr int gathere_minb(int mode) { return (mode == kCheck || mode == kMaskCount || mode == kClamp) ? 5 : 6; }
+// (40 registers; clamp 48)
+constexpr int gathere_minb(int mode) {
+    return (mode == kClamp || (!GD_GATHERE_NARROW && counts(mode))) ? 5 : 6;
+}
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, gathere_minb(MODE)) k_gatherE(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                       uint64_t table, uint64_t idx, uint64_t N, uint32_t D,
@@ -578,8 +586,9 @@ __device__ __forceinline__ void scatter_chunk(const FenceDesc &fd, uint64_t tabl
     }
 }
 
+// 4 CTAs per SM in every mode (64 registers, no local memory)
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, MODE == kMaskCount ? 3 : 4) k_scatter(const __grid_constant__ FenceDesc fd, uint64_t table,
+__global__ void __launch_bounds__(kThreads, 4) k_scatter(const __grid_constant__ FenceDesc fd, uint64_t table,
                                                       uint64_t idx, uint64_t src, uint64_t nvec, uint32_t tail) {
     uint32_t nv = 0;
     EdgeSums es;

@@ -197,7 +197,8 @@ def main():
         # embedding rows: 2^29 u32 table viewed as rows of D words, indices into the row count
         T = 1 << 29
         devmem.view(b, T, torch.int32).random_(generator=gen)
-        for D in (6, 8, 32, 64, 128):                                # D = 6: the flat word kernel k_gatherE
+        Ds = [int(x) for x in os.environ["KB_D"].split(",")] if os.environ.get("KB_D") else (6, 8, 32, 64, 128)
+        for D in Ds:                                                 # D = 6: the flat word kernel k_gatherE
             rows, n = T // D, (1 << 30) // (4 * D)                     # 1 GiB of gathered rows
             devmem.view(b + 2 * GiB + GiB // 2, n, torch.int32).random_(0, rows, generator=gen)
             r = time_modes(lambda m, s: arena.gather(p.id, m, b + 3 * GiB, b, b + 2 * GiB + GiB // 2, n, D, stream=s),
