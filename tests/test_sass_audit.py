@@ -60,7 +60,7 @@ def test_stencil_v2_is_tma_staged(sass):
     assert count(ins, r"LDG") == 0
 
 
-@pytest.mark.parametrize("kernel", ["k_copy", "k_saxpy", "k_gather1", "k_scatter", "k_stencil"])
+@pytest.mark.parametrize("kernel", ["k_copy", "k_saxpy", "k_gather1", "k_gatherE", "k_scatter", "k_stencil"])
 def test_fenced_variants_carry_fence_logic(sass, kernel):
     def key(m):            # k_x<m> or k_x<m, ...> (first instantiation)
         keys = sorted(k for k in sass if k == f"{kernel}<{m}>" or k.startswith(f"{kernel}<{m},"))
