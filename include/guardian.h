@@ -23,7 +23,7 @@
  *  - n = 0 launches are GD_OK and do nothing.
  *  - Size limits (GD_ERR_INVALID_ARG beyond them; every grid stays below
  *    2^31 CTAs): copy n <= 2^44 bytes; saxpy, scatter n <= 2^42 elements;
- *    gather n * row_elems <= 2^42; stencil H * pitch <= 2^58 floats, and
+ *    gather n * row_elems <= 2^41; stencil H * pitch <= 2^58 floats, and
  *    the LSU stencil H <= 2^19 rows (GD_ERR_UNSUPPORTED; the TMA stencil has
  *    no such limit).
  *  - Thread safety: arena mutations (partition alloc/free, malloc/free) are

@@ -571,7 +571,7 @@ gd_status run_work_locked(gd_arena *a, const gd_work &w_in, cudaStream_t stream,
         case GD_KIND_GATHER:
             if ((w.ptr[0] | w.ptr[2]) % 16 || w.ptr[1] % 4) return GD_ERR_ALIGN;
             if (w.u32[0] == 0) return GD_ERR_INVALID_ARG;
-            if (!mul_ok(w.u64[0], (uint64_t)w.u32[0], &t) || t > (1ull << 42)) return GD_ERR_INVALID_ARG;
+            if (!mul_ok(w.u64[0], (uint64_t)w.u32[0], &t) || t > (1ull << 41)) return GD_ERR_INVALID_ARG;   // k_gatherE: 2^11 words per CTA
             bytes = 4 * w.u64[0] + 8 * t;
             empty = w.u64[0] == 0;
             break;

@@ -207,6 +207,7 @@ def test_launch_validation_on_virtual_arena():
     for call in (lambda: a.copy(p.id, "mask", p.base, p.base, (1 << 44) + 16),
                  lambda: a.saxpy(p.id, "mask", 1.0, p.base, p.base, (1 << 42) + 4),
                  lambda: a.gather(p.id, "mask", p.base, p.base, p.base, (1 << 40) + 4, 8),
+                 lambda: a.gather(p.id, "mask", p.base, p.base + 4, p.base, (1 << 40) + 1, 2),   # flat words: 2^41 + 2
                  lambda: a.scatter(p.id, "mask", p.base, p.base, p.base, (1 << 42) + 4)):
         with pytest.raises(g.GuardianError) as e:
             call()
