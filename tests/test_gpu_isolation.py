@@ -60,8 +60,15 @@ def _sanitize(mode, env=None):
     exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     cmd = [exe, "--tool", "memcheck", "--error-exitcode", "9", sys.executable,
            os.path.join(ROOT, "tools", "adversarial.py"), "--mode", mode]
-    return subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
-                          env=dict(os.environ, **(env or {})))
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env=dict(os.environ, **(env or {})))
+    # the GPU pool may wrap compute-sanitizer and refuse to run it (exit 86,
+    # nothing launched): no memcheck evidence on such a box, so skip rather
+    # than read the refusal as a result (test_no_foreign_reads and the
+    # victim-partition checks of every parity test still run)
+    if r.returncode == 86 or "closed on this pool" in r.stdout + r.stderr:
+        pytest.skip("compute-sanitizer is not available on this GPU pool")
+    return r
 
 
 @pytest.mark.parametrize("mode", ["mask", "modulo", "check", "maskcount", "clamp"])
