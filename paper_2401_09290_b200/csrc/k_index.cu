@@ -134,12 +134,16 @@ constexpr uint64_t kEChunk = (uint64_t)kThreads * kE;  // words per CTA
 // pass (two passes per chunk) keep it free of local memory.  GD_GATHERE_NARROW:
 // the check / mask-count passes 4 words wide too, at 6 CTAs per SM instead of
 // 8 words at 5 (D = 6, tools/r02_iter22.sh: check +1.8 -> +0.3 %, mask-count
-// +5.1 -> +0.3 %, per access +6.4 -> +4.2 % / +12.8 -> +7.5 %)
+// +5.1 -> +0.3 %, per access +6.4 -> +4.2 % / +12.8 -> +7.5 %), and modulo
+// (its stream walk spills at 8 words in 40 registers)
 #ifndef GD_GATHERE_NARROW
 #define GD_GATHERE_NARROW 1
 #endif
-constexpr int ke_pass(int mode) { return (mode == kClamp || (GD_GATHERE_NARROW && counts(mode))) ? 4 : kE; }
+constexpr int ke_pass(int mode) { return (mode == kClamp || (GD_GATHERE_NARROW && (counts(mode) || mode == kModulo))) ? 4 : kE; }
 
+#ifndef GD_GATHERE_WALK
+#define GD_GATHERE_WALK 1
+#endif
 // e / D from dinv = floor(2^64 / D), D >= 2 (no 64-bit division call)
 __device__ __forceinline__ uint64_t div_d(uint64_t e, uint32_t D, uint64_t dinv) {
     const uint64_t q = __umul64hi(e, dinv);
@@ -156,18 +160,53 @@ __device__ __forceinline__ void gathere_pass(const FenceDesc &fd, uint64_t out, 
     uint32_t d = (uint32_t)(e0 - i * D);
     int32_t j[KE];
     uint32_t dd[KE];
+    // Modulo on the streams (per access, or a CTA range not inside): this
+    // pass's index and output addresses increase with u, so when neither
+    // range straddles the base nor spans the partition each access's fence
+    // follows from the previous one's (Fence::step_up: one add and one
+    // select, exactly the full modulo, reading A10); otherwise every access
+    // takes the full modulo.
+    bool walk = false;
+    if constexpr (SMODE == kModulo && GD_GATHERE_WALK) {
+        const uint64_t eL = e0 + (uint64_t)(KE - 1) * kThreads;
+        const uint64_t lo_i = idx + 4 * i, hi_i = idx + 4 * div_d(eL, D, dinv) + 4;
+        const uint64_t lo_o = out + 4 * e0, hi_o = out + 4 * eL + 4;
+        const auto side = [&](uint64_t lo, uint64_t hi) {
+            return lo <= hi && hi - lo < fd.size && (hi <= fd.base || lo >= fd.base);
+        };
+        walk = side(lo_i, hi_i) && side(lo_o, hi_o);
+    }
+    if (walk) {
+        uint64_t fa = 0, aa = 0;
 #pragma unroll
-    for (int u = 0; u < KE; u++) {
-        const bool live = e0 + (uint64_t)u * kThreads < N;
-        const uint64_t ai = idx + 4 * i;
-        const bool o = fs.go(ai, nv, (live && d == 0) ? 1u : 0u);
-        j[u] = (int32_t)__ldg(reinterpret_cast<const unsigned int *>(fs.ld_at(fs.addr(ai), o && live)));
-        dd[u] = d;
-        i += qs;
-        d += rs;
-        if (d >= D) {
-            d -= D;
-            i++;
+        for (int u = 0; u < KE; u++) {
+            const bool live = e0 + (uint64_t)u * kThreads < N;
+            const uint64_t ai = idx + 4 * i;
+            fa = u == 0 ? fs.addr(ai) : fs.step_up(fa, ai - aa);
+            aa = ai;
+            j[u] = (int32_t)__ldg(reinterpret_cast<const unsigned int *>(fs.ld_at(fa, live)));
+            dd[u] = d;
+            i += qs;
+            d += rs;
+            if (d >= D) {
+                d -= D;
+                i++;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < KE; u++) {
+            const bool live = e0 + (uint64_t)u * kThreads < N;
+            const uint64_t ai = idx + 4 * i;
+            const bool o = fs.go(ai, nv, (live && d == 0) ? 1u : 0u);
+            j[u] = (int32_t)__ldg(reinterpret_cast<const unsigned int *>(fs.ld_at(fs.addr(ai), o && live)));
+            dd[u] = d;
+            i += qs;
+            d += rs;
+            if (d >= D) {
+                d -= D;
+                i++;
+            }
         }
     }
     uint32_t r[KE];
@@ -177,6 +216,15 @@ __device__ __forceinline__ void gathere_pass(const FenceDesc &fd, uint64_t out, 
         const uint64_t at = table + (uint64_t)((int64_t)j[u] * (int64_t)D + (int64_t)dd[u]) * 4u;
         const bool o = ft.go(at, nv, live ? 1u : 0u);
         r[u] = ld_tab(ft.ld_at(ft.addr(at), o && live));
+    }
+    if (walk) {
+        uint64_t fo = fs.addr(out + 4 * e0);
+#pragma unroll
+        for (int u = 0; u < KE; u++) {
+            if (u) fo = fs.step_up(fo, 4 * kThreads);
+            if (e0 + (uint64_t)u * kThreads < N) st_w(fo, r[u]);
+        }
+        return;
     }
 #pragma unroll
     for (int u = 0; u < KE; u++) {
