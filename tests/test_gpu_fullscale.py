@@ -96,6 +96,70 @@ def test_c3_gather_full(two_tenants, mode):
         assert outs[i] == want, (i, idx[i], outs[i], want)
 
 
+ROW_TAB_OFF, ROW_IDX_OFF, ROW_OUT_OFF, ROW_PAT_OFF = 0, 2 * GiB + GiB // 2, 3 * GiB, 4 * GiB
+
+
+@pytest.mark.parametrize("D", [32, 6])          # k_gatherR (128-bit row slots) / k_gatherE (flat words)
+@pytest.mark.parametrize("mode", ["mask", "check", "maskcount", "clamp", "modulo",
+                                  "check+pa", "modulo+pa", "clamp+pa"])
+def test_row_gather_full(two_tenants, mode, D):
+    """The row gathers in tools/kernel_bench.py's and bench.py's configuration:
+    a 2^29-word table viewed as rows of D words, 1 GiB of gathered rows,
+    1 % planted rows at j in [-2^20, 0) (below the base; mask / modulo wrap
+    them into the top 128 MiB of the partition, which holds the pattern)."""
+    a, victim, p = two_tenants
+    rows, n = T_N // D, GiB // (4 * D)
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(40 + D)
+    devmem.view(p.base + ROW_TAB_OFF, T_N, torch.int32).random_(generator=gen)
+    devmem.view(p.base + ROW_OUT_OFF, n * D, torch.int32).random_(generator=gen)
+    a.fill(p.id, 1, ROW_PAT_OFF, PART - ROW_PAT_OFF)
+    rng = synth.rng_for(4000 + D)
+    j = rng.integers(0, rows, n, dtype=np.int64)
+    pos = synth.planted_positions(rng, n, synth.planted_count(0.01, n))
+    j[pos] = rng.integers(-(1 << 20), 0, len(pos), dtype=np.int64)
+    j = j.astype(np.int32)
+    devmem.view(p.base + ROW_IDX_OFF, n, torch.int32).copy_(torch.from_numpy(j))
+    vview = devmem.view(victim.base, GiB // 4, torch.int32)
+    vcopy = vview.clone()
+    torch.cuda.synchronize()
+    a.stats_reset()
+    a.gather(p.id, mode, p.base + ROW_OUT_OFF, p.base + ROW_TAB_OFF, p.base + ROW_IDX_OFF, n, D)
+    st = a.stats(p.id)
+    out = devmem.view(p.base + ROW_OUT_OFF, n * D, torch.int32).view(n, D)
+    table = devmem.view(p.base + ROW_TAB_OFF, T_N, torch.int32)[: rows * D].view(rows, D)
+    j_t = torch.from_numpy(j.astype(np.int64)).cuda()
+    inb = torch.ones(n, dtype=torch.bool, device="cuda")
+    pos_t = torch.from_numpy(pos).cuda()
+    inb[pos_t] = False
+    # (c) in-bounds rows equal index_select; the victim below is untouched
+    assert torch.equal(out[inb], table[j_t[inb]])
+    assert torch.equal(vview, vcopy)
+    # (a) + (c) planted rows
+    base_mode = mode.split("+")[0]
+    if base_mode == "check":
+        assert st["violations"] == len(pos) * D
+        assert (out[pos_t] == 0).all()
+    elif base_mode == "clamp":                   # every word of a planted row lies below the base: word 0
+        assert st["violations"] == len(pos) * D
+        assert (out[pos_t] == table[0, 0]).all()
+    else:
+        assert st["violations"] == (len(pos) * D if base_mode == "maskcount" else 0)
+        o = np.mod(PART + 4 * (j[pos].astype(np.int64)[:, None] * D + np.arange(D)[None, :]), PART)
+        assert (o >= ROW_PAT_OFF).all()
+        np.testing.assert_array_equal(out[pos_t].cpu().numpy(), synth.pattern_words(o.astype(np.uint64)).view(np.int32))
+    # (b) oracle, one access at a time, on sampled words (planted and in-bounds rows)
+    srng = synth.rng_for(8 + D)
+    rows_s = np.concatenate([srng.choice(pos, 300, replace=False), srng.integers(0, n, 300)])
+    cols_s = srng.integers(0, D, len(rows_s))
+    outs = out.cpu().numpy()
+    for i, d in zip(rows_s, cols_s):
+        a_t = (p.base + ROW_TAB_OFF + 4 * (int(j[i]) * D + int(d))) % 2**64
+        r, ok = oracle.resolve(p.base, p.size, base_mode, a_t, 4)
+        want = 0 if not ok else int(download(r, 4).view(np.int32)[0])
+        assert outs[i, d] == want, (i, d, j[i], outs[i, d], want)
+
+
 @pytest.mark.parametrize("mode", ["mask", "check", "maskcount", "clamp", "modulo",
                                   "check+pa", "maskcount+pa", "clamp+pa", "modulo+pa"])
 def test_c3_scatter_full(two_tenants, mode):
