@@ -38,16 +38,36 @@ __device__ __forceinline__ uint64_t row_addr(uint64_t table, int32_t j) {
 // (A range-only table test, with the one-LOP3 form on >= 4 GiB partitions,
 // measured slower at the L2-resident size: clamp +1.4 -> +11.3 %, per-access
 // check +3.2 -> +4.1 %, tools/r02_iter15.sh; not used.)
+// (table is 4-byte aligned (API) and 4 sext(j) a multiple of 4, so the
+// alignment half of the check predicate is known true: go_aligned)
 template <int MODE>
 __device__ __forceinline__ uint32_t fenced_tab(const Fence<MODE, 4> &f4, uint64_t table, int32_t j, uint32_t &nv) {
     const uint64_t a = row_addr(table, j);
 #if GD_ZERO_REDIRECT
-    const bool o = f4.go(a, nv, 1);
+    const bool o = f4.go_aligned(a, nv, 1);
     return ld_tab(f4.ld_at(f4.addr(a), o));           // refused: the trusted zero block
 #else
-    if (f4.go(a, nv, 1)) return ld_tab(f4.addr(a));
+    if (f4.go_aligned(a, nv, 1)) return ld_tab(f4.addr(a));
     return 0u;
 #endif
+}
+
+// Check / mask-count on a >= 4 GiB power-of-two partition (FenceDesc kBig):
+// the partition test is one LOP3 on the high address word (Fence::in_big), the
+// mask fence another (Fence::addr_big); a refused check load reads the trusted
+// zero block (Fence::ld_at: loading at the mask-fenced address and zeroing the
+// value measured slower, and it moves refused reads to DRAM).  The refusal
+// sets bit `bit` of refm (a compile-time bit: one predicated OR), counted
+// once per chunk.
+template <int MODE>
+__device__ __forceinline__ uint32_t fenced_tab_big(const Fence<MODE, 4> &f4, uint64_t table, int32_t j,
+                                                   uint32_t &refm, int bit) {
+    static_assert(MODE == kCheck || MODE == kMaskCount, "counting mask-type modes");
+    const uint64_t a = row_addr(table, j);
+    const bool in = f4.in_big(a);
+    if (!in) refm |= 1u << bit;
+    if constexpr (MODE == kCheck) return ld_tab(f4.ld_at(a, in));
+    else return ld_tab(f4.addr_big(a));
 }
 
 __device__ __forceinline__ uint64_t chunk_len(uint64_t nvec, uint64_t c0) {
@@ -58,7 +78,7 @@ __device__ __forceinline__ uint64_t chunk_len(uint64_t nvec, uint64_t c0) {
 // K3, D = 1: out[i] = table[sext(idx[i])]
 // SMODE fences the index/output streams, TMODE the table accesses.
 // ---------------------------------------------------------------------------
-template <int SMODE, int TMODE>
+template <int SMODE, int TMODE, bool BIG = false>
 __device__ __forceinline__ void gather_chunk(const FenceDesc &fd, uint64_t out, uint64_t table, uint64_t idx,
                                              uint64_t v0, uint64_t nvec, uint32_t &nv) {
     const Fence<SMODE, 16> f16(fd);
@@ -71,13 +91,27 @@ __device__ __forceinline__ void gather_chunk(const FenceDesc &fd, uint64_t out, 
         if (v < nvec) j[u] = vld4(f16, idx + 16 * v, nv, ld_u4, ld_w);
     }
     uint4 r[kU];
+    if constexpr (BIG) {
+        uint32_t refm = 0;
 #pragma unroll
-    for (int u = 0; u < kU; u++) {
-        if (v0 + u * kThreads < nvec) {
-            r[u].x = fenced_tab<TMODE>(f4, table, (int32_t)j[u].x, nv);
-            r[u].y = fenced_tab<TMODE>(f4, table, (int32_t)j[u].y, nv);
-            r[u].z = fenced_tab<TMODE>(f4, table, (int32_t)j[u].z, nv);
-            r[u].w = fenced_tab<TMODE>(f4, table, (int32_t)j[u].w, nv);
+        for (int u = 0; u < kU; u++) {
+            if (v0 + u * kThreads < nvec) {
+                r[u].x = fenced_tab_big<TMODE>(f4, table, (int32_t)j[u].x, refm, 4 * u);
+                r[u].y = fenced_tab_big<TMODE>(f4, table, (int32_t)j[u].y, refm, 4 * u + 1);
+                r[u].z = fenced_tab_big<TMODE>(f4, table, (int32_t)j[u].z, refm, 4 * u + 2);
+                r[u].w = fenced_tab_big<TMODE>(f4, table, (int32_t)j[u].w, refm, 4 * u + 3);
+            }
+        }
+        nv += __popc(refm);
+    } else {
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            if (v0 + u * kThreads < nvec) {
+                r[u].x = fenced_tab<TMODE>(f4, table, (int32_t)j[u].x, nv);
+                r[u].y = fenced_tab<TMODE>(f4, table, (int32_t)j[u].y, nv);
+                r[u].z = fenced_tab<TMODE>(f4, table, (int32_t)j[u].z, nv);
+                r[u].w = fenced_tab<TMODE>(f4, table, (int32_t)j[u].w, nv);
+            }
         }
     }
 #pragma unroll
@@ -87,6 +121,15 @@ __device__ __forceinline__ void gather_chunk(const FenceDesc &fd, uint64_t out, 
     }
 }
 
+// bit 0: mask-count, bit 1: check take fenced_tab_big on kBig partitions.
+// Mask-count on: L2-resident 2^22 gather per access +1.4 -> +1.2 % (kernel
+// bench), +8.6 -> -0.3 % inside bench.py's process.  Check: no faster (+3.2 %
+// either way per access; loading at the mask-fenced address instead of the
+// zero block: +3.4 -> +14.8 %, and refused reads reach DRAM), off
+// (tools/r02_iter26.sh, r02_iter26b.sh).
+#ifndef GD_GATHER1_BIG
+#define GD_GATHER1_BIG 1
+#endif
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 5) k_gather1(const __grid_constant__ FenceDesc fd, uint64_t out,
                                                       uint64_t table, uint64_t idx, uint64_t nvec, uint32_t tail) {
@@ -94,10 +137,16 @@ __global__ void __launch_bounds__(kThreads, 5) k_gather1(const __grid_constant__
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, v0 = c0 + threadIdx.x;
     if constexpr (hoistable(MODE)) {     // streams hoisted; random table accesses fenced
         const uint64_t cn = chunk_len(nvec, c0);
-        if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, out + 16 * c0, 16 * cn))
+        constexpr bool kBigTab = (MODE == kMaskCount && (GD_GATHER1_BIG & 1)) || (MODE == kCheck && (GD_GATHER1_BIG & 2));
+        const bool inside = cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, out + 16 * c0, 16 * cn);
+        if (kBigTab && (fd.flags & kBig)) {
+            if (inside) gather_chunk<kNone, MODE, kBigTab>(fd, out, table, idx, v0, nvec, nv);
+            else gather_chunk<MODE, MODE, kBigTab>(fd, out, table, idx, v0, nvec, nv);
+        } else if (inside) {
             gather_chunk<kNone, MODE>(fd, out, table, idx, v0, nvec, nv);
-        else
+        } else {
             gather_chunk<MODE, MODE>(fd, out, table, idx, v0, nvec, nv);
+        }
     } else {
         gather_chunk<MODE, MODE>(fd, out, table, idx, v0, nvec, nv);
     }
