@@ -5,7 +5,7 @@
 # the LSU stencil and the row gather), the kernel bench of every kernel in ten
 # modes.  Output in gpurun_out/r02final/.
 cd "$(dirname "$0")/.."
-O=gpurun_out/r02final2; mkdir -p $O
+O=${O:-gpurun_out/r02final2}; mkdir -p $O
 nvidia-smi --query-gpu=name,memory.total,clocks.max.sm,clocks.sm,power.limit --format=csv > $O/gpuinfo.txt 2>&1
 if [ -z "$SKIP_SUITES" ]; then
 timeout 1500 python -m pytest -q -p no:cacheprovider -m gpu tests --durations=15 > $O/pytest.log 2>&1
