@@ -36,6 +36,8 @@
 // concurrent tenants never share it; a placement past its slice's run (only
 // possible if the tenant rewrites idx while its own launch runs) is dropped,
 // never written outside the scratch.
+#include <type_traits>
+
 #include "fence.cuh"
 #include "kernels.h"
 
@@ -80,11 +82,28 @@ __device__ __forceinline__ void edge_add(const FenceDesc &fd, const EdgeAcc &es)
 // One RMW of the direct kernel's semantics, resolved: *word = partition word
 // offset of the fenced address when it is to be bucketed (returns true);
 // otherwise counted / clamped / (NONE, outside) applied directly in pass 1.
-template <int MODE, int PASS>
+// NEAR (modulo, decided per launch: the table base lies in the partition and
+// the partition is at least 2^33 bytes): every RMW offset a - base = (table -
+// base) + 4 sext(j) lies in [-2^33, 2 size), so its u64 remainder (reading
+// A10) needs at most one correction: s >= 0: s or s - size; s < 0: the u64
+// value 2^64 + s has remainder (c + s) mod size with c = 2^64 mod size, i.e.
+// c + s or c + s + size.  Exactly the full modulo, without the reciprocal.
+template <int MODE, int PASS, bool NEAR = false>
 __device__ __forceinline__ bool resolve(const Fence<MODE, 4> &f4, uint64_t table, int32_t j, uint32_t v,
-                                        uint32_t &nv, EdgeAcc &es, uint64_t &word) {
+                                        uint32_t &nv, EdgeAcc &es, uint64_t &word, uint64_t c64 = 0) {
     const uint64_t a = table + (uint64_t)((int64_t)j * 4);        // sext, scale in 64 bits (Listing 1 l.22)
-    if constexpr (MODE == kNone) {
+    if constexpr (MODE == kModulo && NEAR) {
+        const uint64_t off = a - f4.base;
+        uint64_t r;
+        if ((int64_t)off >= 0) {
+            r = off >= f4.size ? off - f4.size : off;
+        } else {
+            const uint64_t x = off + c64;                            // c + s, as u64
+            r = (int64_t)x < 0 ? x + f4.size : x;
+        }
+        word = r >> 2;                                               // (r & ~3) / 4: a is 4-aligned
+        return true;
+    } else if constexpr (MODE == kNone) {
         if (a - f4.base <= f4.lim && (a & 3) == 0) {
             word = (a - f4.base) >> 2;
             return true;
@@ -123,13 +142,14 @@ __device__ __forceinline__ bool resolve(const Fence<MODE, 4> &f4, uint64_t table
 // bucketed at partition word w[k], rank rk[k] in its slice's CTA histogram.
 constexpr int kItems = 4 * kU;
 
-template <int SMODE, int MODE, int PASS>
+template <int SMODE, int MODE, int PASS, bool NEAR = false>
 __device__ __forceinline__ void items(const FenceDesc &fd, uint64_t table, uint64_t idx, uint64_t src, uint64_t v0,
                                       uint64_t nvec, uint32_t &nv, EdgeAcc &es, unsigned *hist,
                                       uint32_t (&w)[kItems], uint32_t (&rk)[kItems], uint32_t (&sv)[kItems],
                                       uint32_t &putm) {
     const Fence<SMODE, 16> f16(fd);
     const Fence<MODE, 4> f4(fd);
+    const uint64_t c64 = NEAR ? 0ull - fd.inv * fd.size : 0ull;   // 2^64 mod size (inv = floor(2^64 / size))
     uint4 j[kU], s[kU];
     // Every load of the 2 kU is issued unconditionally, with no branch
     // between them (a branch per vector had made ptxas consume each loaded
@@ -194,7 +214,7 @@ __device__ __forceinline__ void items(const FenceDesc &fd, uint64_t table, uint6
         for (int q = 0; q < 4; q++) {
             const int k = 4 * u + q;
             uint64_t word = 0;
-            const bool put = live && resolve<MODE, PASS>(f4, table, (int32_t)jj[q], ss[q], nv, es, word);
+            const bool put = live && resolve<MODE, PASS, NEAR>(f4, table, (int32_t)jj[q], ss[q], nv, es, word, c64);
             w[k] = (uint32_t)word;
             sv[k] = ss[q];
             rk[k] = put ? atomicAdd(&hist[w[k] >> (kSliceShift - 2)], 1u) : 0u;
@@ -216,15 +236,25 @@ __global__ void __launch_bounds__(kThreads) k_scatter_part(const __grid_constant
     uint32_t w[kItems], rk[kItems], sv[kItems];
     EdgeAcc es;
     const uint64_t c0 = (uint64_t)blockIdx.x * kChunk, v0 = c0 + threadIdx.x;
-    if constexpr (hoistable(MODE)) {                   // streams hoisted per CTA tile; RMWs fenced one by one
-        const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
-        if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, src + 16 * c0, 16 * cn))
-            items<kNone, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
-        else
-            items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
-    } else {
-        items<MODE, MODE, PASS>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
-    }
+    const auto run = [&](auto near_tag) {
+        constexpr bool NEAR = decltype(near_tag)::value;
+        if constexpr (hoistable(MODE)) {               // streams hoisted per CTA tile; RMWs fenced one by one
+            const uint64_t cn = nvec > c0 ? (nvec - c0 < kChunk ? nvec - c0 : kChunk) : 0;
+            if (cn && range_in(fd, idx + 16 * c0, 16 * cn) && range_in(fd, src + 16 * c0, 16 * cn))
+                items<kNone, MODE, PASS, NEAR>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
+            else
+                items<MODE, MODE, PASS, NEAR>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
+        } else {
+            items<MODE, MODE, PASS, NEAR>(fd, table, idx, src, v0, nvec, nv, es, hist, w, rk, sv, putm);
+        }
+    };
+#ifndef GD_SCATTER_MOD_NEAR
+#define GD_SCATTER_MOD_NEAR 1
+#endif
+    if (MODE == kModulo && GD_SCATTER_MOD_NEAR && table - fd.base < fd.size && fd.size >= (1ull << 33))
+        run(std::true_type{});
+    else
+        run(std::false_type{});
     __syncthreads();
     if constexpr (PASS == 0) {
         for (uint32_t i = threadIdx.x; i < nslices; i += kThreads)

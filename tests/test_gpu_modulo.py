@@ -244,3 +244,63 @@ def test_modulo_equals_mask_on_pow2_partition(arenas):
         a.gather(p.id, mode, p.base + 6 * MiB, p.base, p.base + 4 * MiB, n)
         outs.append(download(p.base + 6 * MiB, 4 * n))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("mode", ["modulo", "modulo+pa"])
+def test_modulo_scatter_near_large_exact_partition(arenas, mode):
+    """The scatter-add's near modulo (a table inside a partition of >= 2^33
+    bytes: one correction instead of the reciprocal, k_scatter.cu resolve) on
+    a non-power-of-two 8 GiB + 14 MiB partition, through the bucketed path,
+    with the table 4 GiB into the partition: in-bounds updates, updates past
+    the end (offsets in [size + 2 GiB, size + 3 GiB)) and below the base
+    (s < 0: the u64 remainder of 2^64 + s, reading A10, which is not the
+    Euclidean one for this size).  Every update's word comes from the
+    oracle's fence; the partition must equal `before` plus their index_add,
+    word for word."""
+    import torch
+    from paper_2401_09290_b200 import devmem
+    GiB = 1 << 30
+    size = 8 * GiB + 14 * MiB
+    a = arenas(16 * GiB)
+    p = a.partition_alloc_exact(size)
+    assert p.size == size and not p.pow2
+    tab_off, idx_off, src_off = 4 * GiB, GiB, GiB + 8 * MiB
+
+    def addr(j):                                       # table + 4 sext(j), mod 2^64
+        return np.uint64(p.base + tab_off) + (4 * np.asarray(j, dtype=np.int64)).astype(np.uint64)
+
+    rng = synth.rng_for(617)
+    n = (1 << 20) + 4
+    T = 1 << 28                                        # in-bounds words: [4 GiB, 5 GiB)
+    j = rng.integers(0, T, n, dtype=np.int64)
+    k = synth.planted_count(0.02, n)
+    pos = synth.planted_positions(rng, n, k)
+    hi, lo = pos[: k // 2], pos[k // 2:]
+    j[hi] = (size - 2 * GiB) // 4 + rng.integers(0, GiB // 4, len(hi))        # past the end
+    cand = rng.integers(-(1 << 31), -(1 << 30), 8 * len(lo))                    # below the base
+    land = oracle.fence_modulo_n(addr(cand), p.base, size, 4) - np.uint64(p.base)
+    keep = cand[land >= np.uint64(2 * GiB)]                                      # clear of idx / src
+    assert len(keep) >= len(lo)
+    j[lo] = keep[: len(lo)]
+    off = addr(j) - np.uint64(p.base)
+    assert (off[hi] >= np.uint64(size)).all() and (off[lo] > np.uint64(1 << 63)).all()
+    jv = j.astype(np.int32)
+    src = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    devmem.view(p.base + idx_off, n, torch.int32).copy_(torch.from_numpy(jv))
+    devmem.view(p.base + src_off, n, torch.int32).copy_(torch.from_numpy(src.view(np.int32)))
+    whole = devmem.view(p.base, size // 4, torch.int32)
+    whole[tab_off // 4: tab_off // 4 + T].random_(generator=torch.Generator(device="cuda:0").manual_seed(5))
+    before = whole.clone()
+    a.stats_reset()
+    a.scatter(p.id, mode, p.base + tab_off, p.base + idx_off, p.base + src_off, n)
+    assert a.stats(p.id)["violations"] == 0
+    words = (oracle.fence_modulo_n(addr(jv), p.base, size, 4) - np.uint64(p.base)) // np.uint64(4)
+    w_t = torch.from_numpy(words.astype(np.int64)).cuda()
+    s_t = torch.from_numpy(src.astype(np.int64)).cuda()
+    u, inv = torch.unique(w_t, return_inverse=True)
+    sums = torch.zeros(u.numel(), dtype=torch.int64, device="cuda").index_add_(0, inv, s_t)
+    want = (before[u].long() + sums) & 0xFFFFFFFF
+    assert torch.equal(whole[u].long() & 0xFFFFFFFF, want)
+    after = whole.clone()
+    after[u] = before[u]
+    assert torch.equal(after, before)
