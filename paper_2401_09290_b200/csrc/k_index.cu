@@ -188,7 +188,9 @@ constexpr uint64_t kEChunk = (uint64_t)kThreads * kE;  // words per CTA
 #ifndef GD_GATHERE_NARROW
 #define GD_GATHERE_NARROW 1
 #endif
-constexpr int ke_pass(int mode) { return (mode == kClamp || (GD_GATHERE_NARROW && (counts(mode) || mode == kModulo))) ? 4 : kE; }
+constexpr int ke_pass(int mode) {
+    return (mode == kClamp || (GD_GATHERE_NARROW && (counts(mode) || mode == kModulo))) ? 4 : kE;
+}
 
 #ifndef GD_GATHERE_WALK
 #define GD_GATHERE_WALK 1
