@@ -358,6 +358,14 @@ __global__ void __launch_bounds__(kThreads, gathere_minb(MODE)) k_gatherE(const 
 #ifndef GD_GATHER_CLAMP_REDIRECT
 #define GD_GATHER_CLAMP_REDIRECT 0x0
 #endif
+// CLAMP_BITS (bit G): step 3b takes each outside vector's edge word from a
+// below-the-base bit instead of the vector's address, so the addresses die at
+// their loads; with it the fix-up fits behind one branch (CLAMP_FIX_BRANCH)
+// at G = 2 without local memory: D = 64 clamp +9.6-10.0 -> +0.0-0.1 %
+// (tools/r02_iter28.sh; G = 4 measured no faster per access, G = 1 spills).
+#ifndef GD_GATHER_CLAMP_BITS
+#define GD_GATHER_CLAMP_BITS 0x4
+#endif
 #ifndef GD_GATHER_LIVE_REDIRECT
 #define GD_GATHER_LIVE_REDIRECT 1
 #endif
@@ -466,6 +474,9 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     uint64_t at[S][G];
     bool ok[S][G];
     uint32_t cnt[S];
+    // clamp (GD_GATHER_CLAMP_BITS): bit k*G+g set when that vector lies below
+    // the base, so step 3b needs only bits, not the vectors' addresses
+    uint32_t below = 0;
 #pragma unroll
     for (int k = 0; k < S; k++) {                       // 2. fenced table addresses (ALU only)
         const int32_t jk = ((SMODE == kClamp && !kClampSafe) || okj[k]) ? j[k] : 0;   // a refused index load reads 0
@@ -495,6 +506,7 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
                 at[k][g] = a;
                 ok[k][g] = (a - fd.base) <= fd.size - 16;
                 cnt[k] += ok[k][g] ? 0u : 4u;
+                if (((GD_GATHER_CLAMP_BITS >> G) & 1) && a < fd.base) below |= 1u << (k * G + g);
             } else {
                 at[k][g] = ft.addr(a);
                 ok[k][g] = ft.go_aligned(a, cnt[k], 4);
@@ -522,15 +534,16 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
     }
     if constexpr (TMODE == kClamp) {                    // 3b. rare: outside vectors, after every load issued
 #ifndef GD_GATHER_CLAMP_FIX_BRANCH
-#define GD_GATHER_CLAMP_FIX_BRANCH 0x0
+#define GD_GATHER_CLAMP_FIX_BRANCH 0x4
 #endif
         // (bit G of CLAMP_FIX_BRANCH: one branch around the whole fix-up, taken
         // only when some vector of the thread lies outside; else predicated
-        // edge-word loads per vector.  Off: at G = 2 and 1 it makes ptxas
-        // spill within the 6-CTA register budget.  The D = 64 clamp gather
-        // stays +6-11 % over its twin, against 0-1 % for every other mode:
-        // measured variants -- index loads from a safe word, no warp sync,
-        // table loads from the zero block -- all 6-47 %, tools/r02_iter11.sh)
+        // edge-word loads per vector, which every warp issues.  On at G = 2
+        // with CLAMP_BITS (without them ptxas spills within the 6-CTA
+        // register budget); off at G = 1 (spills).  Before it the D = 64 clamp
+        // gather stayed +6-11 % over its twin: index loads from a safe word,
+        // no warp sync, table loads from the zero block all measured 6-47 %,
+        // tools/r02_iter11.sh)
         bool anyout = !((GD_GATHER_CLAMP_FIX_BRANCH >> G) & 1);
 #pragma unroll
         for (int k = 0; k < S; k++)
@@ -542,7 +555,10 @@ __device__ __forceinline__ void gatherr_chunk(const FenceDesc &fd, uint64_t out,
 #pragma unroll
                 for (int g = 0; g < G; g++) {
                     if (live[k] && !ok[k][g]) {
-                        const uint32_t w = ld_tab(ft.edge4(at[k][g]));
+                        const uint64_t e = ((GD_GATHER_CLAMP_BITS >> G) & 1)
+                                               ? (((below >> (k * G + g)) & 1u) ? fd.base : fd.base + fd.size - 4)
+                                               : ft.edge4(at[k][g]);
+                        const uint32_t w = ld_tab(e);
                         r[k][g] = make_uint4(w, w, w, w);
                     }
                 }
